@@ -1,0 +1,382 @@
+"""Benchmark of the B200 Sinkhorn-WMD hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+A step is one full query solve — cost/kernel build, max_iter fused
+iterations, final pass — over the configured synthetic corpus
+(paper_2107_06433_b200.synth; seeded stand-ins for the paper's datasets).
+At N=1 the workload is BASELINE.json configs[1] ("c2": V=100k, N=5k docs,
+v_r=19, fp64, lam=10, 15 iterations).  With --gpus N>1 (torchrun, NCCL) the
+corpus grows to N x 5k documents and is column-sharded, one block per rank
+("scaling": "weak"); the distances are all-gathered inside every timed step.
+
+Metric: nnz*iterations/s of the whole solve (higher is better); docs/s beside it.
+  value  device-resident inputs, CUDA events on the solver stream, L2 flushed
+         (256 MiB write) before every step, max over ranks;
+  e2e    the public API sinkhorn_wmd(query ndarray, corpus, E, config) per step:
+         query selection on the host, H2D of (sel, r), kernels, D2H of the
+         distances + error record; corpus and E resident (uploaded once).
+
+--impl reference times the reference algorithm on the host cores (the
+oracle/ C port of sinkwmd's numba kernels, deterministic column-block mode,
+all hardware threads) on the same config; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "Sinkhorn-WMD nnz*iters/s per query (docs/s beside it)"
+UNIT = "nnz*iters/s"
+
+
+def _peaks() -> dict:
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def start(self):
+        self._t.start()
+        return self
+
+    def stop(self) -> dict:
+        self._stop.set()
+        self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _config(name: str, world: int):
+    from paper_2107_06433_b200 import synth
+
+    cfg = synth.CONFIGS[name]
+    n_docs = cfg.n_docs * world if name in ("c1", "c2") else cfg.n_docs
+    scaling = "weak" if name in ("c1", "c2") else "strong"
+    return cfg, n_docs, scaling
+
+
+def _workload_json(cfg, n_docs, nnz, world, scaling, flush: bool):
+    return {
+        "workload": f"{cfg.name}: V={cfg.n_vocab} N={n_docs} docs ({cfg.k_min}-{cfg.k_max} "
+                    f"Zipf({cfg.zipf_s}) words each), v_r={cfg.v_r}, w={cfg.dim}, "
+                    f"lam={cfg.lam}, max_iter={cfg.max_iter}, seed={cfg.seed}",
+        "nnz": int(nnz),
+        "n_docs": int(n_docs),
+        "parallelism": f"column shards x{world}" if world > 1 else "1 GPU",
+        "scaling_mode": scaling,
+        "l2": "flushed (256 MiB write) before every step" if flush else "warm",
+    }
+
+
+# ---------------------------------------------------------------------------------------------
+
+def run_reference(args):
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2107_06433_b200 import synth
+
+    cfg, n_docs, scaling = _config(args.config, world)
+    inst = synth.zipf_instance(cfg, n_docs=n_docs)
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    run = lambda: oracle.solve(inst.query, inst.col_ptr, inst.rows, inst.vals,  # noqa: E731
+                               inst.embeddings, lam=cfg.lam, max_iter=cfg.max_iter, blocks=cores)
+    for _ in range(args.warmup):
+        run()
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    wall = time.perf_counter() - t_all
+    ms = 1e3 * wall / args.steps
+    value = inst.nnz * cfg.max_iter * args.steps / wall
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Zipf corpus, Gaussian embeddings)",
+        "config": _workload_json(cfg, n_docs, inst.nnz, world, scaling, False),
+        "docs_per_s": n_docs * args.steps / wall,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"full {cfg.name} solve x{args.steps} (oracle/swmd_oracle.c, "
+                                   f"deterministic column blocks, {cores} OpenMP threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _cpu_baseline(inst, cfg) -> dict:
+    """Rank 0, N=1: the oracle port on the host cores over a bounded sample."""
+    import oracle
+
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    oracle.solve(inst.query, inst.col_ptr, inst.rows, inst.vals, inst.embeddings,
+                 lam=cfg.lam, max_iter=cfg.max_iter, blocks=cores)
+    reps, t_total = 0, 0.0
+    while reps < 20 and t_total < 8.0:
+        t0 = time.perf_counter()
+        oracle.solve(inst.query, inst.col_ptr, inst.rows, inst.vals, inst.embeddings,
+                     lam=cfg.lam, max_iter=cfg.max_iter, blocks=cores)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    return {"value": inst.nnz * cfg.max_iter * reps / t_total, "unit": UNIT, "cores": cores,
+            "kind": "port",
+            "sample": f"{reps} full {cfg.name} solves, {t_total:.2f}s (oracle/swmd_oracle.c, "
+                      f"{cores} OpenMP threads, deterministic column blocks)"}
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_06433_b200 as swmd
+    from paper_2107_06433_b200 import _lib, synth
+    from paper_2107_06433_b200.device import DeviceCorpus, DeviceEmbeddings, stream_ptr
+    from paper_2107_06433_b200.distributed import DeviceShardSolver, shard_bounds, sinkhorn_wmd_sharded
+    from paper_2107_06433_b200.solver import QueryPlan, SinkhornWorkspace
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, n_docs, scaling = _config(args.config, world)
+    inst = synth.zipf_instance(cfg, n_docs=n_docs)
+    corpus = inst.corpus()
+    scfg = swmd.SolverConfig(lam=cfg.lam, max_iter=cfg.max_iter)
+    sel, weights = swmd.select_nonzero(inst.query)
+    bounds = shard_bounds(corpus, world)
+    c0, c1 = int(bounds[rank]), int(bounds[rank + 1])
+    solver = DeviceShardSolver(corpus, inst.embeddings, dev=dev)
+    solver(sel, weights, c0, c1, scfg, None)              # upload the block, build the plan
+    dc = solver._blocks[(c0, c1)]
+    de = DeviceEmbeddings.of(inst.embeddings, dev)
+    ws = solver.ws
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    s = stream_ptr(dev)
+    width = int(np.max(np.diff(bounds)))
+    gather_in = torch.zeros(width, dtype=torch.float64, device=dev)
+    gather_out = torch.zeros(width * world, dtype=torch.float64, device=dev)
+
+    def device_step(plan, ev=None):
+        if ev is not None:
+            ev[0].record()
+        plan.enqueue_distances()
+        if ev is not None:
+            ev[1].record()
+        plan.enqueue_solve()
+        if ev is not None:
+            ev[2].record()
+        if world > 1:
+            gather_in[: c1 - c0].copy_(plan.wmd)
+            dist.all_gather_into_tensor(gather_out, gather_in)
+        if ev is not None:
+            ev[3].record()
+
+    plan = QueryPlan(sel, weights, dc, de, scfg, ws)
+    for _ in range(max(args.warmup, 3)):
+        device_step(plan)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local).start() if rank == 0 else None
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    plan.launches = 0
+    for k in range(args.steps):
+        if args.flush:
+            _lib.call("swmd_l2_flush", flush_buf.data_ptr(), flush_buf.numel(), s)
+        device_step(plan, evs[k])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clock_info = clocks.stop() if clocks else None
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    cost_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    solve_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    launches = plan.launches
+    tot_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    # the plan's result must still be right: check the last step against a fresh solve
+    wmd_dev = plan.wmd.clone()
+
+    # e2e through the public API (corpus, E resident; query in, distances out)
+    for _ in range(2):
+        if world > 1:
+            sinkhorn_wmd_sharded(inst.query, corpus, inst.embeddings, scfg, solver=solver)
+        else:
+            swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, scfg, workspace=ws)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if world > 1:
+            res = sinkhorn_wmd_sharded(inst.query, corpus, inst.embeddings, scfg, solver=solver)
+        else:
+            res = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, scfg, workspace=ws)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert np.array_equal(res.wmd[c0:c1], wmd_dev.cpu().numpy()), "device-timed result drifted"
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    nnz_all = inst.nnz
+    iters = cfg.max_iter
+    value = nnz_all * iters * args.steps / (tot_ms / 1e3)
+    ms_step = tot_ms / args.steps
+    peaks = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    # algorithmic bytes of the two kernels
+    v_r = int(sel.size)
+    rows_built = dc.n_present if dc.n_present < dc.n_rows else dc.n_rows
+    cost_bytes = rows_built * (cfg.dim * 8 + 8) + 2 * rows_built * v_r * 8
+    nnz_loc = dc.nnz
+    # the survey's canonical per-iteration HBM figure (x round trip counted; "effective"
+    # for the persistent kernel, which keeps x on chip)
+    it_bytes = nnz_loc * 12 + 2 * dc.n_cols * v_r * 8 + 4 * (dc.n_cols + 1)
+    fin_bytes = nnz_loc * 12 + dc.n_cols * v_r * 8 + dc.n_cols * 8 + 4 * (dc.n_cols + 1)
+    solve_bytes = iters * it_bytes + fin_bytes
+    c_ms, s_ms = float(np.mean(cost_ms)), float(np.mean(solve_ms))
+    gather_l2 = nnz_loc * v_r * 8 * (iters + 2)          # K-row gathers (+KM in the final)
+    flops = iters * (4 * nnz_loc * v_r + 2 * nnz_loc + dc.n_cols * v_r) + 6 * nnz_loc * v_r
+    dominant = "solve" if s_ms >= c_ms else "cost"
+    if dominant == "solve":
+        achieved = solve_bytes / (s_ms / 1e3) / 1e9
+        traffic = None
+    else:
+        achieved = cost_bytes / (c_ms / 1e3) / 1e9
+        traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Zipf corpus, Gaussian embeddings; paper datasets absent)",
+        "config": _workload_json(cfg, n_docs, nnz_all, world, scaling, args.flush),
+        "docs_per_s": n_docs * args.steps / (tot_ms / 1e3),
+        "roofline": {
+            "bound": "hbm", "kernel": "swmd_solve_f64 (persistent fused loop)" if dominant == "solve"
+            else "swmd_cost_build_f64",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback",
+            "traffic": traffic,
+            "bytes_per_launch": solve_bytes if dominant == "solve" else cost_bytes,
+            "note": ("solve bytes = survey §8d B_HBM per iteration x iterations + final "
+                     "(x round trip counted although the persistent kernel keeps x on chip: "
+                     "an effective figure)") if dominant == "solve" else
+                    "cost bytes = E rows of words present in the corpus + K, K*M writes",
+        },
+        "kernels": {
+            "cost_build_ms": c_ms, "cost_build_gbs": cost_bytes / (c_ms / 1e3) / 1e9,
+            "solve_ms": s_ms, "solve_eff_hbm_gbs": solve_bytes / (s_ms / 1e3) / 1e9,
+            "solve_gather_gbs": gather_l2 / (s_ms / 1e3) / 1e9,
+            "solve_fp64_gflops": flops / (s_ms / 1e3) / 1e9,
+            "rows_built": int(rows_built),
+        },
+        "e2e": {"value": nnz_all * iters * args.steps / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(2 * v_r * 8),
+                "d2h_bytes_per_step": int((dc.n_cols + _lib.ERR_WORDS) * 8),
+                "ms_per_step": 1e3 * e2e_s / args.steps,
+                "note": "public sinkhorn_wmd(); corpus and embeddings resident in HBM"},
+        "gpu_launches": int(launches),
+        "clocks": clock_info,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = _cpu_baseline(inst, cfg)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-flush", dest="flush", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,171 @@
+/*
+ * swmd.h — C ABI of the B200 (sm_100a) Sinkhorn-WMD hot path (libswmd.so).
+ *
+ * Every entry point replaces one native kernel of the reference package
+ * (/root/reference/pkg/src/sinkwmd/_jit.py, called from kernels.py / solver.py)
+ * and keeps its calling convention: plain pointers and sizes, caller-owned
+ * buffers mutated in place, errors reported through an out-parameter rather
+ * than exceptions.  Differences, all forced by the device boundary:
+ *
+ *   - every pointer except `err` readbacks is DEVICE memory (cudaMalloc /
+ *     torch CUDA tensors); every call is asynchronous on the caller's stream
+ *     (`stream` is a cudaStream_t, NULL = legacy default stream);
+ *   - the corpus arrives column-major (CSC: col_ptr int64, rows int32
+ *     ascending inside a column, vals f64), i.e. the reference's
+ *     CsrMatrix.csc_index() view (sparse.py:98-120) — the traversal of its
+ *     deterministic "columns" mode (_jit.py:164-183);
+ *   - the reference's errpos (2,) int64 becomes a device int64[SWMD_ERR_WORDS]
+ *     record, reset by swmd_err_reset and read back by the host, which raises
+ *     the reference's DegeneracyError messages (kernels.py:170-174,
+ *     solver.py:95-103).
+ *
+ * Return value: 0 on success, a cudaError_t value on a CUDA failure, or one
+ * of the SWMD_E* codes below for an argument the kernels cannot take.
+ */
+#ifndef SWMD_H
+#define SWMD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWMD_ABI_VERSION 1
+
+#define SWMD_EINVAL 1000      /* bad size / null pointer / misaligned buffer */
+#define SWMD_EVR 1001         /* v_r outside what this entry point supports */
+
+/*
+ * Error record (device int64[SWMD_ERR_WORDS]); "no event" is INT64_MAX.
+ *   err[0]  min over zero denominators of (code << 47) | (i * n_key + j)
+ *           — the smallest (i, j) in row-major order, i.e. the pair the
+ *           reference's serial CSR walk reports first (_jit.py:130-134);
+ *           (i * n_key + j) saturates at 2^47-1 (host then re-derives).
+ *   err[1]  min event code of a nonpositive iterate entry (update_u check);
+ *   err[2]  max |x_new - x_prev| as the bit pattern of a nonnegative double
+ *           (tol path; reset to 0);
+ *   err[3]  min event code at which an iterate entry was NaN.
+ * Event codes order the reference's checks inside one solve: iteration t
+ * performs update_u on x^(t) (code 2t) then the fused iteration (2t+1); the
+ * final pass is update_u on x^(T) (code 2T) then fused_final (2T+1).
+ */
+#define SWMD_ERR_WORDS 4
+
+int swmd_abi_version(void);
+int swmd_device_sm_count(void);
+int swmd_err_reset(int64_t* err, void* stream);
+
+/* Row sums of squares of E (V x dim, row stride ldE) — cached per embedding
+ * table for the Gram-form cost build. */
+int swmd_row_norms_f64(const double* E, int64_t V, int32_t dim, int64_t ldE,
+                       double* norms, void* stream);
+
+/*
+ * Cost + Gibbs-kernel build for one query: replaces _jit.euclid_rows
+ * (_jit.py:90-102, called by kernels.euclidean_rows, kernels.py:91-111) fused
+ * with _jit.precompute_mats (_jit.py:105-114, kernels.precompute,
+ * kernels.py:114-141).  For each row i (all V rows, or the n_list rows in
+ * row_list) and query word a < v_r:
+ *     M[i,a]  = ||E[sel[a]] - E[i]||_2
+ *     K[i,a]  = exp(-lam * M[i,a]);  KoR = K / weights[a];  KM = K * M
+ * Outputs are (V, ldk) row-major, ldk >= v_r; columns a in [v_r, ldk) are
+ * written as 0.  Any of cost / kernel_over_r / kernel_cost may be NULL.
+ * mode 0: difference form in the reference's exact operation order
+ *         (no FMA): bitwise-identical M.
+ * mode 1: Gram form ||e||^2 + ||q||^2 - 2 e.q on FMA (norms required),
+ *         M[sel[a],a] forced to exactly 0 and near-zero distances
+ *         recomputed in difference form.
+ */
+int swmd_cost_build_f64(const double* E, int64_t V, int32_t dim, int64_t ldE,
+                        const int64_t* sel, int32_t v_r, const double* weights,
+                        double lam, int32_t mode, const double* norms,
+                        const int32_t* row_list, int64_t n_list,
+                        double* cost, double* kernel, double* kernel_over_r,
+                        double* kernel_cost, int64_t ldk, void* stream);
+
+/* Elementwise precompute from a given cost matrix: replaces
+ * _jit.precompute_mats (_jit.py:105-114) behind kernels.precompute
+ * (kernels.py:114-141).  kernel_over_r / kernel_cost may be NULL. */
+int swmd_precompute_f64(const double* cost, int64_t V, int32_t v_r, int64_t ldk,
+                        const double* weights, double lam, double* kernel,
+                        double* kernel_over_r, double* kernel_cost, void* stream);
+
+/*
+ * The whole Sinkhorn loop for one query over a CSC column range, in ONE
+ * persistent launch: replaces the solver loop of solver.py:168-193 —
+ * update_u (solver.py:95-103) + _jit.fused_iter_columns (_jit.py:164-183)
+ * per iteration and update_u + _jit.fused_final_columns (_jit.py:291-312)
+ * at the end.  Columns are independent (test_acceptance.py:212-222), so
+ * each column runs all of its iterations with x, u held on chip; v is never
+ * stored.  kernel_over_r is folded: x[j,a] = (sum_i K[i,a] t_ij) / r[a].
+ *   iterations t_begin <= t < t_end run; x_in (N x v_r) seeds x^(t_begin)
+ *   (NULL = the reference's init 1/v_r); x_out (nullable) receives x^(t_end);
+ *   wmd (nullable) receives the final pass; delta_out on err[2] when x_in
+ *   is given (tol path).  order (nullable) is a column permutation used as
+ *   the work order (longest columns first).  counter is a device int32
+ *   scratch word (reset inside).  col_key_offset / n_key place the local
+ *   columns in the global (i * n_key + j) error key.  group_hint = lanes per
+ *   column for v_r <= 32 (16 or 32; 32 suits columns longer than ~64).
+ * Supports any v_r >= 1 (v_r <= 32 on the register-resident fast kernel).
+ */
+int swmd_solve_f64(const int64_t* col_ptr, const int32_t* rows, const double* vals,
+                   int64_t n_cols, const int32_t* order,
+                   const double* kernel, const double* kernel_cost,
+                   const double* weights, int32_t v_r, int64_t ldk,
+                   int32_t t_begin, int32_t t_end,
+                   const double* x_in, double* x_out, double* wmd,
+                   int64_t col_key_offset, int64_t n_key, int32_t group_hint,
+                   int64_t* err, int32_t* counter, void* stream);
+
+/*
+ * One fused type-1 iteration with explicit u and kernel_over_r, accumulating
+ * into x (x[j,a] += sum ...; zero it first for a fresh iteration):
+ * replaces _jit.fused_iter_serial / _columns (_jit.py:120-137, 164-183) as
+ * called by kernels.fused_iteration (kernels.py:250-310).  Per column the
+ * accumulation runs over rows in increasing order (the reference's order).
+ * Zero denominators: event code 1.
+ */
+int swmd_fused_iteration_f64(const int64_t* col_ptr, const int32_t* rows,
+                             const double* vals, int64_t n_cols,
+                             const double* kernel, const double* kernel_over_r,
+                             int32_t v_r, int64_t ldk, const double* u, double* x,
+                             int64_t n_key, int64_t* err, void* stream);
+
+/* Type-2 final pass with explicit u: wmd[j] = sum (c/(K_i.u_j)) (KM_i.u_j);
+ * replaces _jit.fused_final_* (_jit.py:243-312) behind kernels.fused_final
+ * (kernels.py:313-354).  wmd is overwritten.  Zero denominators: code 1. */
+int swmd_fused_final_f64(const int64_t* col_ptr, const int32_t* rows,
+                         const double* vals, int64_t n_cols,
+                         const double* kernel, const double* kernel_cost,
+                         int32_t v_r, int64_t ldk, const double* u, double* wmd,
+                         int64_t n_key, int64_t* err, void* stream);
+
+/* Unfused SDDMM: w[pos[q]] = vals[q] / (K[rows[q],:] . u[j,:]) with w in CSR
+ * storage order (pos = CsrMatrix.csc_index()[2]); replaces _jit.sddmm_*
+ * (_jit.py:319-358) behind kernels.sddmm (kernels.py:177-208).  A zero
+ * denominator stores 0 and records code 1. */
+int swmd_sddmm_f64(const int64_t* col_ptr, const int32_t* rows, const int64_t* pos,
+                   const double* vals, int64_t n_cols, const double* kernel,
+                   int32_t v_r, int64_t ldk, const double* u, double* w,
+                   int64_t n_key, int64_t* err, void* stream);
+
+/* Unfused SpMM: x[j,:] += sum_q kernel_over_r[rows[q],:] * w[pos[q]];
+ * replaces _jit.spmm_* (_jit.py:361-398) behind kernels.spmm
+ * (kernels.py:211-247).  Rows in increasing order per column. */
+int swmd_spmm_f64(const int64_t* col_ptr, const int32_t* rows, const int64_t* pos,
+                  const double* w, int64_t n_cols, const double* kernel_over_r,
+                  int32_t v_r, int64_t ldk, double* x, void* stream);
+
+/* u = 1/x elementwise with the update_u check (solver.py:95-103): records
+ * `code` in err[1] if any entry <= 0 and in err[3] if any entry is NaN. */
+int swmd_update_u_f64(const double* x, double* u, int64_t n, int32_t code,
+                      int64_t* err, void* stream);
+
+/* Flush helper for benchmarks: writes `bytes` of scratch (L2 eviction). */
+int swmd_l2_flush(void* scratch, int64_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWMD_H */

@@ -1,0 +1,348 @@
+"""Parity of the sm_100a path with the reference (golden fixtures) and the CPU oracle.
+
+Tolerances: fp64 distances within 1e-9 relative (BASELINE.json north_star),
+top-k identical; kernel-level pieces far tighter (stated per test).  Every
+call goes through libswmd.so.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import column_subset, golden, max_rel_err, small_instance
+
+import paper_2107_06433_b200 as swmd
+from paper_2107_06433_b200 import synth
+from paper_2107_06433_b200.sparse import CsrMatrix, csr_from_triplets
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    swmd.kernels.warmup()
+
+
+def _topk_equal(got, want, k):
+    a = np.argsort(got, kind="stable")[:k]
+    b = np.argsort(want, kind="stable")[:k]
+    if np.array_equal(a, b):
+        return True
+    # a flip is only legitimate between near-ties of the reference
+    srt = np.sort(want)
+    return bool(np.any(np.abs(np.diff(srt[: k + 1])) <= RTOL * np.abs(srt[1: k + 1])))
+
+
+# -- kernel level, against the reference's own outputs (small.npz) -------------------------
+
+def test_euclidean_rows_bitwise(small_golden):
+    g = small_golden
+    for k in range(50):
+        q, corpus, emb = small_instance(g, k)
+        sel = np.flatnonzero(q > 0)
+        got = swmd.euclidean_rows(emb, sel)
+        assert np.array_equal(got, g[f"i{k}_cost"]), k
+
+
+def test_euclidean_rows_gram_mode(small_golden):
+    g = small_golden
+    for k in range(50):
+        q, corpus, emb = small_instance(g, k)
+        sel = np.flatnonzero(q > 0)
+        got = swmd.euclidean_rows(emb, sel, mode=swmd.kernels.COST_MODE_GRAM)
+        want = g[f"i{k}_cost"]
+        assert np.all(got[sel, np.arange(sel.size)] == 0.0)
+        nz = want > 0
+        assert np.all(np.abs(got[nz] - want[nz]) <= 1e-12 * want[nz]), k
+
+
+def test_precompute_and_invariants(small_golden):
+    g = small_golden
+    for k in range(50):
+        q, corpus, emb = small_instance(g, k)
+        sel = np.flatnonzero(q > 0)
+        mats = swmd.precompute(g[f"i{k}_cost"], q[sel], 10.0)
+        # CUDA exp is within 1 ulp of glibc exp
+        assert max_rel_err(mats.kernel, g[f"i{k}_kernel"]) <= 4.5e-16
+        assert max_rel_err(mats.kernel_over_r, g[f"i{k}_kor"]) <= 7e-16
+        assert max_rel_err(mats.kernel_cost, g[f"i{k}_kcost"]) <= 7e-16
+        assert np.array_equal(mats.kernel == 1.0, mats.cost == 0.0)
+        assert np.all(mats.kernel > 0) and np.all(mats.kernel <= 1.0)
+
+
+def test_fused_iteration_final_sddmm_spmm(small_golden, oracle_lib):
+    g = small_golden
+    for k in range(50):
+        p = f"i{k}_"
+        q, corpus, emb = small_instance(g, k)
+        mats = swmd.SinkhornMatrices(g[p + "cost"], g[p + "kernel"], g[p + "kor"],
+                                     g[p + "kcost"], 10.0)
+        u = g[p + "u"]
+        x = np.zeros_like(u)
+        swmd.fused_iteration(corpus, mats, u, x)
+        assert max_rel_err(x, g[p + "x1"]) <= 1e-13, k
+        assert max_rel_err(swmd.fused_final(corpus, mats, u), g[p + "final"]) <= 1e-13, k
+        w = swmd.sddmm(corpus, mats.kernel, u)
+        assert max_rel_err(w, g[p + "sddmm"]) <= 1e-14, k
+        xs = swmd.spmm(corpus, g[p + "sddmm"], mats.kernel_over_r)
+        want = oracle_lib.spmm_serial(corpus.row_ptr, corpus.col_idx, g[p + "sddmm"],
+                                      mats.kernel_over_r, corpus.n_cols)
+        assert max_rel_err(xs, want) <= 1e-14, k
+
+
+def test_fused_equals_composition(small_golden):
+    g = small_golden
+    q, corpus, emb = small_instance(g, 3)
+    p = "i3_"
+    mats = swmd.SinkhornMatrices(g[p + "cost"], g[p + "kernel"], g[p + "kor"], g[p + "kcost"], 10.0)
+    u = g[p + "u"]
+    fused = np.zeros_like(u)
+    swmd.fused_iteration(corpus, mats, u, fused)
+    composed = swmd.spmm(corpus, swmd.sddmm(corpus, mats.kernel, u), mats.kernel_over_r)
+    assert max_rel_err(fused, composed) <= 1e-14
+
+
+def test_work_count(small_golden):
+    g = small_golden
+    q, corpus, emb = small_instance(g, 5)
+    p = "i5_"
+    mats = swmd.SinkhornMatrices(g[p + "cost"], g[p + "kernel"], g[p + "kor"], g[p + "kcost"], 10.0)
+    u = g[p + "u"]
+    c1 = np.zeros(1, dtype=np.int64)
+    swmd.fused_iteration(corpus, mats, u, np.zeros_like(u), counts=c1)
+    assert c1[0] == 2 * corpus.nnz * mats.v_r
+    c3 = np.zeros(3, dtype=np.int64)
+    swmd.fused_iteration(corpus, mats, u, np.zeros_like(u), workers=3, counts=c3)
+    assert c3.sum() == 2 * corpus.nnz * mats.v_r
+    with pytest.raises(ValueError, match="deterministic"):
+        swmd.fused_iteration(corpus, mats, u, np.zeros_like(u), workers=2, deterministic=True,
+                             counts=c3[:2])
+
+
+def test_zero_denominator_named():
+    corpus = csr_from_triplets([(0, 0, 1.0)], 1, 1)
+    mats = swmd.SinkhornMatrices(np.zeros((1, 1)), np.array([[0.0]]), np.array([[0.0]]),
+                                 np.array([[0.0]]), 1.0)
+    with pytest.raises(swmd.DegeneracyError, match=r"\(0, 0\)"):
+        swmd.sddmm(corpus, mats.kernel, np.array([[1.0]]))
+    with pytest.raises(swmd.DegeneracyError, match=r"zero denominator at nonzero \(0, 0\)"):
+        swmd.fused_iteration(corpus, mats, np.array([[1.0]]), np.zeros((1, 1)))
+
+
+# -- solver, against the reference's solver outputs -------------------------------------------------
+
+def test_small_solver(small_golden):
+    g = small_golden
+    worst = 0.0
+    for k in range(50):
+        q, corpus, emb = small_instance(g, k)
+        for lam in (1, 10):
+            got = swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig(lam=float(lam))).wmd
+            worst = max(worst, max_rel_err(got, g[f"i{k}_wmd_lam{lam}"]))
+    assert worst <= RTOL, worst
+
+
+@pytest.mark.parametrize("mode", ["gram", "direct"])
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_config_parity(name, mode):
+    g = golden(name)
+    inst = synth.zipf_instance(name)
+    cfg = swmd.SolverConfig(lam=10.0, max_iter=15, cost_mode=mode)
+    res = swmd.sinkhorn_wmd(inst.query, inst.corpus(), inst.embeddings, cfg)
+    err = max_rel_err(res.wmd, g["wmd"])
+    assert err <= RTOL, err
+    for k in (10, 100):
+        assert _topk_equal(res.wmd, g["wmd"], k)
+    assert res.iterations_run == 15 and not res.converged
+    assert set(res.timings) == {"select", "distances", "precompute", "init", "iterations",
+                                "final", "total"}
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_large_config_parity(name):
+    g = golden(name)
+    inst = synth.zipf_instance(name)
+    res = swmd.sinkhorn_wmd(inst.query, inst.corpus(), inst.embeddings,
+                            swmd.SolverConfig(lam=10.0, max_iter=15))
+    stride = int(g["sample_stride"])
+    assert max_rel_err(res.wmd[::stride], g["sample"]) <= RTOL
+    order = np.argsort(res.wmd, kind="stable")
+    top = g["top100"]
+    assert max_rel_err(res.wmd[top], g["top100_wmd"]) <= RTOL
+    assert np.array_equal(order[:100], top) or _topk_equal(res.wmd[top], g["top100_wmd"], 100)
+    assert abs(float(np.sum(res.wmd)) - float(g["wmd_sum"])) <= RTOL * abs(float(g["wmd_sum"]))
+
+
+@pytest.mark.parametrize("v_r", [1, 2, 3, 4, 5, 7, 8, 12, 13, 16, 19, 20, 24, 27, 31, 32,
+                                 33, 48, 64, 100, 300])
+def test_query_length_buckets(v_r, oracle_lib):
+    rng = np.random.default_rng(100 + v_r)
+    V, N = 3000, 150
+    emb = synth.normal_embeddings(rng, V, 64)
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, 5, 40)
+    q = synth.zipf_query(rng, V, v_r)
+    corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+    got = swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig(lam=10.0, max_iter=15)).wmd
+    want = oracle_lib.solve(q, cp, rows, vals, emb, lam=10.0, max_iter=15).wmd
+    assert max_rel_err(got, want) <= RTOL
+
+
+@pytest.mark.parametrize("kmin,kmax", [(1, 3), (90, 200), (300, 420)])
+def test_column_length_regimes(kmin, kmax, oracle_lib):
+    """Short columns, columns past the register cache (>96 nonzeros) and the
+    32-lanes-per-column regime."""
+    rng = np.random.default_rng(kmin)
+    V, N = 4000, 120
+    emb = synth.normal_embeddings(rng, V, 32)
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, kmin, kmax)
+    corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+    for v_r in (6, 19):
+        q = synth.zipf_query(rng, V, v_r)
+        got = swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig()).wmd
+        want = oracle_lib.solve(q, cp, rows, vals, emb).wmd
+        assert max_rel_err(got, want) <= RTOL
+
+
+# -- acceptance criteria & solver contracts (test_acceptance.py, test_solver.py) -------------
+
+def test_analytic_singletons():
+    vecs = np.array([[0.0, 0.0], [1.0, 0.0]])
+    query = np.array([1.0, 0.0])
+    cfg = swmd.SolverConfig(lam=1.0, max_iter=15)
+    same = csr_from_triplets([(0, 0, 1.0)], 2, 1)
+    apart = csr_from_triplets([(1, 0, 1.0)], 2, 1)
+    assert abs(swmd.sinkhorn_wmd(query, same, vecs, cfg).wmd[0]) <= 1e-12
+    assert abs(swmd.sinkhorn_wmd(query, apart, vecs, cfg).wmd[0] - 1.0) <= 1e-12
+    res = swmd.sinkhorn_wmd(query, same, vecs, swmd.SolverConfig(lam=1.0, max_iter=15, tol=1e-12))
+    assert abs(res.wmd[0]) <= 1e-12 and res.converged and res.iterations_run == 1
+    one = swmd.sinkhorn_wmd(query, apart, vecs, swmd.SolverConfig(lam=1.0, max_iter=1))
+    assert abs(one.wmd[0] - 1.0) <= 1e-12
+
+
+def test_zero_column_degenerates_cleanly(oracle_lib):
+    corpus = csr_from_triplets([(0, 0, 1.0)], 2, 2)  # column 1 empty
+    vecs = np.array([[0.0, 0.0], [1.0, 0.0]])
+    with pytest.raises(swmd.DegeneracyError) as exc:
+        swmd.sinkhorn_wmd(np.array([1.0, 0.0]), corpus, vecs, swmd.SolverConfig(lam=1.0, max_iter=3))
+    cp, rows, _, vals = corpus.csc_index()
+    with pytest.raises(oracle_lib.OracleDegeneracy) as want:
+        oracle_lib.solve(np.array([1.0, 0.0]), cp, rows, vals, vecs, lam=1.0, max_iter=3)
+    assert str(exc.value) == str(want.value)
+
+
+def test_zero_denominator_in_solver_matches_oracle(oracle_lib):
+    # lam large enough that exp(-lam*M) underflows to 0 for far words
+    rng = np.random.default_rng(9)
+    V, N = 50, 12
+    emb = rng.normal(size=(V, 4)) * 30
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, 2, 5)
+    corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+    q = np.zeros(V)
+    q[[3, 7]] = [0.5, 0.5]
+    cfg = swmd.SolverConfig(lam=50.0, max_iter=4)
+    with pytest.raises(swmd.DegeneracyError) as exc:
+        swmd.sinkhorn_wmd(q, corpus, emb, cfg)
+    with pytest.raises(oracle_lib.OracleDegeneracy) as want:
+        oracle_lib.solve(q, cp, rows, vals, emb, lam=50.0, max_iter=4)
+    assert str(exc.value) == str(want.value)
+
+
+def test_tol_exit_is_self_consistent():
+    inst = synth.zipf_instance("c1", n_docs=40)
+    corpus = inst.corpus()
+    tol = 1e-9
+    res = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings,
+                            swmd.SolverConfig(lam=1.0, max_iter=500, tol=tol))
+    assert res.converged and res.iterations_run < 500
+    more = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings,
+                             swmd.SolverConfig(lam=1.0, max_iter=res.iterations_run + 1, tol=tol))
+    assert more.iterations_run == res.iterations_run
+    assert np.array_equal(more.wmd, res.wmd)
+    # the per-iteration (tol) path and the persistent path compute the same bits
+    fixed = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings,
+                              swmd.SolverConfig(lam=1.0, max_iter=res.iterations_run))
+    assert np.array_equal(fixed.wmd, res.wmd)
+
+
+def test_column_independence_bitwise():
+    inst = synth.zipf_instance("c1", n_docs=120)
+    corpus = inst.corpus()
+    cfg = swmd.SolverConfig()
+    full = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
+    cols = np.random.default_rng(777).choice(120, size=17, replace=False)
+    part = swmd.sinkhorn_wmd(inst.query, column_subset(corpus, cols), inst.embeddings, cfg).wmd
+    assert np.array_equal(part, full[cols])
+
+
+def test_shard_counts_bitwise():
+    """Column blocks solved separately (the multi-GPU shards) reassemble to the
+    single-launch result bit for bit, for 1/2/4/8 shards."""
+    from paper_2107_06433_b200.distributed import DeviceShardSolver, shard_bounds
+
+    inst = synth.zipf_instance("c2", n_docs=3000)
+    corpus = inst.corpus()
+    cfg = swmd.SolverConfig()
+    full = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
+    sel, w = swmd.select_nonzero(inst.query)
+    solver = DeviceShardSolver(corpus, inst.embeddings)
+    for world in (1, 2, 4, 8):
+        b = shard_bounds(corpus, world)
+        out = np.concatenate([solver(sel, w, int(b[r]), int(b[r + 1]), cfg, None).wmd
+                              for r in range(world)])
+        assert np.array_equal(out, full), world
+
+
+def test_batch_and_workspace():
+    inst = synth.zipf_instance("c1", n_docs=50)
+    corpus = inst.corpus()
+    rng = np.random.default_rng(71)
+    queries = [synth.zipf_query(rng, inst.n_vocab, v) for v in (3, 7, 19, 40)]
+    cfg = swmd.SolverConfig()
+    batch = swmd.sinkhorn_wmd_batch(queries + [np.zeros(inst.n_vocab)], corpus,
+                                    inst.embeddings, cfg)
+    for qv, r in zip(queries, batch):
+        alone = swmd.sinkhorn_wmd(qv, corpus, inst.embeddings, cfg)
+        assert np.array_equal(r.wmd, alone.wmd)
+    assert isinstance(batch[-1], swmd.EmptyQueryError)
+    ws = swmd.SinkhornWorkspace()
+    first = swmd.sinkhorn_wmd(queries[2], corpus, inst.embeddings, cfg, workspace=ws)
+    snap = first.wmd.copy()
+    swmd.sinkhorn_wmd(queries[0], corpus, inst.embeddings, cfg, workspace=ws)
+    again = swmd.sinkhorn_wmd(queries[2], corpus, inst.embeddings, cfg, workspace=ws)
+    assert np.array_equal(first.wmd, snap) and np.array_equal(again.wmd, first.wmd)
+
+
+def test_sparse_vector_query_and_embedding_cache():
+    inst = synth.zipf_instance("c1", n_docs=30)
+    corpus = inst.corpus()
+    cfg = swmd.SolverConfig()
+    idx = np.flatnonzero(inst.query)
+    dense = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
+    sparse = swmd.sinkhorn_wmd(swmd.SparseVector(inst.n_vocab, idx, inst.query[idx]), corpus,
+                               inst.embeddings, cfg).wmd
+    assert np.array_equal(dense, sparse)
+    # an in-place edit of a cached embedding table is picked up
+    emb = inst.embeddings.copy()
+    a = swmd.sinkhorn_wmd(inst.query, corpus, emb, cfg).wmd
+    emb[:] = emb[::-1]
+    b = swmd.sinkhorn_wmd(inst.query, corpus, emb, cfg).wmd
+    c = swmd.sinkhorn_wmd(inst.query, corpus, emb.copy(), cfg).wmd
+    assert not np.array_equal(a, b) and np.array_equal(b, c)
+
+
+def test_torch_cuda_embeddings():
+    import torch
+
+    inst = synth.zipf_instance("c1", n_docs=30)
+    corpus = inst.corpus()
+    cfg = swmd.SolverConfig()
+    a = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
+    b = swmd.sinkhorn_wmd(inst.query, corpus, torch.from_numpy(inst.embeddings).cuda(), cfg).wmd
+    assert np.array_equal(a, b)

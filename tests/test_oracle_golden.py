@@ -1,0 +1,100 @@
+"""Pin the CPU oracle (oracle/swmd_oracle.c) to outputs of the reference itself.
+
+The fixtures in tests/golden/ were produced by the reference package
+(tests/golden/make_golden.py imports /root/reference/pkg/src/sinkwmd).  The
+oracle restates the reference's numba kernels in C with the same operation
+order and no FMA contraction, so every comparison here is BITWISE.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden, small_instance
+
+from paper_2107_06433_b200 import synth
+
+
+def _fp(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def test_small_kernels_bitwise(small_golden, oracle_lib):
+    g = small_golden
+    o = oracle_lib
+    for k in range(50):
+        p = f"i{k}_"
+        q, corpus, emb = small_instance(g, k)
+        sel = np.flatnonzero(q > 0)
+        cost = o.euclid_rows(emb, sel)
+        assert np.array_equal(cost, g[p + "cost"]), k
+        kern, kor, kcost = o.precompute(cost, q[sel], 10.0)
+        assert np.array_equal(kern, g[p + "kernel"]), k
+        assert np.array_equal(kor, g[p + "kor"]), k
+        assert np.array_equal(kcost, g[p + "kcost"]), k
+        u = g[p + "u"]
+        x = o.fused_iter_serial(corpus.row_ptr, corpus.col_idx, corpus.values, kern, kor, u)
+        assert np.array_equal(x, g[p + "x1"]), k
+        wf = o.fused_final_serial(corpus.row_ptr, corpus.col_idx, corpus.values, kern, kcost, u)
+        assert np.array_equal(wf, g[p + "final"]), k
+        w = o.sddmm_serial(corpus.row_ptr, corpus.col_idx, corpus.values, kern, u)
+        assert np.array_equal(w, g[p + "sddmm"]), k
+        # the column-block traversal equals the CSR traversal bitwise
+        cp, rows, _, vals = corpus.csc_index()
+        xc = o.fused_iter_columns(cp, rows, vals, kern, kor, u, blocks=3)
+        assert np.array_equal(xc, x), k
+
+
+def test_small_solver_bitwise(small_golden, oracle_lib):
+    g = small_golden
+    for k in range(50):
+        q, corpus, emb = small_instance(g, k)
+        cp, rows, _, vals = corpus.csc_index()
+        for lam in (1, 10):
+            res = oracle_lib.solve(q, cp, rows, vals, emb, lam=float(lam), max_iter=15, blocks=2)
+            assert np.array_equal(res.wmd, g[f"i{k}_wmd_lam{lam}"]), (k, lam)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_config_full_bitwise(name, oracle_lib):
+    g = golden(name)
+    inst = synth.zipf_instance(name)
+    assert _fp(inst.col_ptr, inst.rows, inst.vals) == str(g["fp_corpus"])
+    assert _fp(inst.query) == str(g["fp_query"])
+    assert _fp(inst.embeddings) == str(g["fp_embeddings"])
+    res = oracle_lib.solve(inst.query, inst.col_ptr, inst.rows, inst.vals, inst.embeddings,
+                           lam=inst.config.lam, max_iter=inst.config.max_iter)
+    assert np.array_equal(res.wmd, g["wmd"])
+
+
+def test_c3_sampled_bitwise(oracle_lib):
+    g = golden("c3")
+    inst = synth.zipf_instance("c3")
+    assert _fp(inst.col_ptr, inst.rows, inst.vals) == str(g["fp_corpus"])
+    res = oracle_lib.solve(inst.query, inst.col_ptr, inst.rows, inst.vals, inst.embeddings,
+                           lam=10.0, max_iter=15)
+    stride = int(g["sample_stride"])
+    assert np.array_equal(res.wmd[::stride], g["sample"])
+    order = np.argsort(res.wmd, kind="stable")
+    assert np.array_equal(order[:100], g["top100"])
+    assert float(np.sum(res.wmd)) == float(g["wmd_sum"])
+
+
+def test_column_blocks_match_reference_semantics(oracle_lib):
+    from paper_2107_06433_b200.sparse import column_blocks
+
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        lens = rng.integers(0, 9, size=int(rng.integers(1, 40)))
+        cp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+        for p in (1, 2, 3, 5, 8, 64):
+            assert np.array_equal(oracle_lib.column_blocks(cp, p), column_blocks(cp, p))
