@@ -106,7 +106,8 @@ int swmd_precompute_f64(const double* cost, int64_t V, int32_t v_r, int64_t ldk,
  *   the work order (longest columns first).  counter is a device int32
  *   scratch word (reset inside).  col_key_offset / n_key place the local
  *   columns in the global (i * n_key + j) error key.  group_hint = lanes per
- *   column for v_r <= 32 (16 or 32; 32 suits columns longer than ~64).
+ *   column for the register-only v_r <= 32 kernel (16 or 32); max_len_hint =
+ *   longest column (sizes the shared-memory slab of staged K rows; 0 = 96).
  * Supports any v_r >= 1 (v_r <= 32 on the register-resident fast kernel).
  */
 int swmd_solve_f64(const int64_t* col_ptr, const int32_t* rows, const double* vals,
@@ -116,7 +117,7 @@ int swmd_solve_f64(const int64_t* col_ptr, const int32_t* rows, const double* va
                    int32_t t_begin, int32_t t_end,
                    const double* x_in, double* x_out, double* wmd,
                    int64_t col_key_offset, int64_t n_key, int32_t group_hint,
-                   int64_t* err, int32_t* counter, void* stream);
+                   int32_t max_len_hint, int64_t* err, int32_t* counter, void* stream);
 
 /*
  * One fused type-1 iteration with explicit u and kernel_over_r, accumulating

@@ -47,7 +47,7 @@ _SIGS = {
                             _P, _P, _P, _P, _I64, _P],
     "swmd_precompute_f64": [_P, _I64, _I32, _I64, _P, _D, _P, _P, _P, _P],
     "swmd_solve_f64": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
-                       _I64, _I64, _I32, _P, _P, _P],
+                       _I64, _I64, _I32, _I32, _P, _P, _P],
     "swmd_fused_iteration_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _P],
     "swmd_fused_final_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _P],
     "swmd_sddmm_f64": [_P, _P, _P, _P, _I64, _P, _I32, _I64, _P, _P, _I64, _P, _P],

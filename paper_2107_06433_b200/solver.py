@@ -205,7 +205,7 @@ def _nonpositive_entry(dc: DeviceCorpus, K, KM, r_dev, v_r: int, ldk: int, t_che
                   dc.n_cols, dc.order.data_ptr(), K.data_ptr(), KM.data_ptr(), r_dev.data_ptr(),
                   v_r, ldk, t, t + 1, cur.data_ptr() if cur is not None else None,
                   nxt.data_ptr(), None, dc.col_offset, dc.n_key, _group(dc, v_r),
-                  err.data_ptr(), counter.data_ptr(), stream_ptr(dev))
+                  dc.max_len, err.data_ptr(), counter.data_ptr(), stream_ptr(dev))
         cur = nxt
     x = cur.view(dc.n_cols, v_r)
     # global flat index in the reference's (N, v_r) iterate
@@ -256,7 +256,9 @@ class QueryPlan:
         self.dev = dc.device
         self.dws = dws = ws.on(self.dev)
         v_r = self.v_r = int(sel.size)
-        self.ldk = v_r + (v_r & 1)          # even row stride: 16-byte K rows
+        # K row stride = v_r rounded up to 4 (zero pad columns): 16-byte rows that
+        # the fast v_r <= 32 kernel reads as whole pairs without masking
+        self.ldk = ((v_r + 3) // 4) * 4 if v_r <= 32 else v_r + (v_r & 1)
         V, N = dc.n_rows, dc.n_cols
         stage = ws.pinned("qstage", 2 * v_r, torch.int64)
         stage_np = stage.numpy()
@@ -301,7 +303,8 @@ class QueryPlan:
                   x_in.data_ptr() if x_in is not None else None,
                   x_out.data_ptr() if x_out is not None else None,
                   wmd.data_ptr() if wmd is not None else None, dc.col_offset, dc.n_key,
-                  self.group, self.err.data_ptr(), self.counter.data_ptr(), self.stream)
+                  self.group, dc.max_len, self.err.data_ptr(), self.counter.data_ptr(),
+                  self.stream)
         self.launches += 1
 
     def enqueue_solve(self) -> None:
