@@ -12,7 +12,7 @@ corpus grows to N x 5k documents and is column-sharded, one block per rank
 
 Metric: nnz*iterations/s of the whole solve (higher is better); docs/s beside it.
   value  device-resident inputs, CUDA events on the solver stream, L2 flushed
-         (256 MiB write) before every step, max over ranks;
+         (256 MiB scratch written, then read back) before every step, max over ranks;
   e2e    the public API sinkhorn_wmd(query ndarray, corpus, E, config) per step:
          query selection on the host, H2D of (sel, r), kernels, D2H of the
          distances + error record; corpus and E resident (uploaded once).
@@ -51,7 +51,8 @@ def _peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled (every 20 ms, one
+    nvidia-smi process in loop mode) during the timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -59,39 +60,41 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.samples: list[list[str]] = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.05)
+        self.proc = None
 
     def start(self):
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
         return self
 
     def stop(self) -> dict:
-        self._stop.set()
-        self._t.join(timeout=10)
-        if not self.samples:
+        if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        samples = [[v.strip() for v in ln.split(",")] for ln in out.splitlines() if ln.strip()]
+        samples = [x for x in samples if len(x) >= 7]
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        num = lambda v: float(v) if v.replace(".", "").isdigit() else None  # noqa: E731
+        sm = [num(x[0]) for x in samples if num(x[0]) is not None]
+        mx = [num(x[1]) for x in samples if num(x[1]) is not None]
+        busy = [num(x[0]) for x in samples if num(x[6]) and num(x[6]) > 0 and num(x[0])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        reasons = sorted({names[k] for x in samples for k in range(4)
+                          if x[2 + k].lower() == "active"})
+        med = statistics.median(busy) if busy else (statistics.median(sm) if sm else None)
+        return {"sm_mhz": med, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(samples), "samples_busy": len(busy)}
 
 
 def _dist_env():
@@ -119,7 +122,8 @@ def _workload_json(cfg, n_docs, nnz, world, scaling, flush: bool):
         "n_docs": int(n_docs),
         "parallelism": f"column shards x{world}" if world > 1 else "1 GPU",
         "scaling_mode": scaling,
-        "l2": "flushed (256 MiB write) before every step" if flush else "warm",
+        "l2": ("flushed before every step: 256 MiB scratch written then read back "
+               "(L2 holds no solver data and no dirty lines)") if flush else "warm",
     }
 
 
@@ -313,12 +317,20 @@ def run_b200(args):
     gather_l2 = nnz_loc * v_r * 8 * (iters + 2)          # K-row gathers (+KM in the final)
     flops = iters * (4 * nnz_loc * v_r + 2 * nnz_loc + dc.n_cols * v_r) + 6 * nnz_loc * v_r
     dominant = "solve" if s_ms >= c_ms else "cost"
+    ncu = {}
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_ncu.json")) as f:
+            ncu = json.load(f)["kernels"]
+    except (OSError, KeyError, ValueError):
+        pass
+    kname = "hybrid_solve" if dominant == "solve" else "cost_dmma_kernel"
+    traffic = None
+    if kname in ncu and args.config == "c2" and world == 1:
+        traffic = ncu[kname]["dram_read_bytes"] + ncu[kname]["dram_write_bytes"]
     if dominant == "solve":
         achieved = solve_bytes / (s_ms / 1e3) / 1e9
-        traffic = None
     else:
         achieved = cost_bytes / (c_ms / 1e3) / 1e9
-        traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -332,6 +344,8 @@ def run_b200(args):
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback",
             "traffic": traffic,
+            "traffic_source": "profiles/r01_ncu.json (ncu --set full, dram read+write bytes per launch)"
+            if traffic is not None else None,
             "bytes_per_launch": solve_bytes if dominant == "solve" else cost_bytes,
             "note": ("solve bytes = survey §8d B_HBM per iteration x iterations + final "
                      "(x round trip counted although the persistent kernel keeps x on chip: "
@@ -364,7 +378,7 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])

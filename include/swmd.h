@@ -163,7 +163,18 @@ int swmd_spmm_f64(const int64_t* col_ptr, const int32_t* rows, const int64_t* po
 int swmd_update_u_f64(const double* x, double* u, int64_t n, int32_t code,
                       int64_t* err, void* stream);
 
-/* Flush helper for benchmarks: writes `bytes` of scratch (L2 eviction). */
+/* HOST function: the query's positive entries (kernels.select_nonzero,
+ * kernels.py:74-88) in one pass over the dense histogram r (n doubles).
+ * Writes the ascending word ids to stage[0:cnt] and the weights (float64
+ * bit patterns) to stage[cnt:2*cnt]; stage holds 2*cap int64.  Returns cnt,
+ * -2 if an entry is negative (ValueError), -1 on bad arguments, or the
+ * needed cap (> cap) when stage is too small.  cnt == 0 means no positive
+ * entry (EmptyQueryError). */
+int64_t swmd_select_query(const double* r, int64_t n, int64_t* stage, int64_t cap);
+
+/* Flush helper for benchmarks: writes `bytes` of scratch (> L2 evicts
+ * everything) and reads it back, leaving L2 clean (no dirty write-back is
+ * charged to the next kernel). */
 int swmd_l2_flush(void* scratch, int64_t bytes, void* stream);
 
 #ifdef __cplusplus

@@ -54,7 +54,9 @@ _SIGS = {
     "swmd_spmm_f64": [_P, _P, _P, _P, _I64, _P, _I32, _I64, _P, _P],
     "swmd_update_u_f64": [_P, _P, _I64, _I32, _P, _P],
     "swmd_l2_flush": [_P, _I64, _P],
+    "swmd_select_query": [_P, _I64, _P, _I64],
 }
+_RESTYPE = {"swmd_select_query": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGS)
 
@@ -69,7 +71,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     for name, argtypes in _SIGS.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = ctypes.c_int
+        fn.restype = _RESTYPE.get(name, ctypes.c_int)
     return lib
 
 

@@ -24,6 +24,7 @@ Per-phase times come from CUDA events on the solver's stream.
 from __future__ import annotations
 
 import time
+from collections.abc import Mapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -35,6 +36,7 @@ from .kernels import (
     COST_MODE_DIRECT,
     COST_MODE_GRAM,
     DegeneracyError,
+    EmptyQueryError,
     raise_zero_denominator,
     select_nonzero,
     zero_denominator_event,
@@ -132,9 +134,22 @@ class SinkhornWorkspace:
     def pinned(self, name: str, n: int, dtype=torch.int64) -> torch.Tensor:
         p = self._pinned.get(name)
         if p is None or p.numel() < n or p.dtype != dtype:
-            p = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+            # pinned when a device exists (async H2D); plain host memory otherwise,
+            # so argument errors still surface before the missing-device error
+            p = torch.empty(max(n, 1), dtype=dtype, pin_memory=torch.cuda.is_available())
             self._pinned[name] = p
+            self._pinned_np = {}
         return p[:n]
+
+    def pinned_np(self, name: str, n: int) -> np.ndarray:
+        """numpy view of a pinned int64 staging buffer (grow-only)."""
+        t = self.pinned(name, n)
+        cache = self.__dict__.setdefault("_pinned_np", {})
+        arr = cache.get(name)
+        if arr is None or arr.size < n:
+            arr = self._pinned[name].numpy()
+            cache[name] = arr
+        return arr
 
 
 def init_x(v_r: int, n_docs: int) -> np.ndarray:
@@ -170,6 +185,8 @@ def _default_ws() -> SinkhornWorkspace:
 
 
 class _Events:
+    """CUDA events on the solver stream; spans resolve lazily (LazyTimings)."""
+
     def __init__(self, enabled: bool):
         self.enabled = enabled
         self.ev: dict[str, torch.cuda.Event] = {}
@@ -184,6 +201,38 @@ class _Events:
         if not self.enabled or a not in self.ev or b not in self.ev:
             return 0.0
         return self.ev[a].elapsed_time(self.ev[b]) / 1e3
+
+
+class LazyTimings(Mapping):
+    """The reference's per-phase timings dict (solver.py:131-194).  Device
+    phases are CUDA-event spans resolved on first access, so a solve does not
+    pay for event queries nobody reads."""
+
+    def __init__(self, host: dict, spans: dict, events: _Events):
+        self._host = host
+        self._spans = spans
+        self._events = events
+        self._resolved: dict | None = None
+
+    def _all(self) -> dict:
+        if self._resolved is None:
+            d = dict(self._host)
+            for k, v in self._spans.items():
+                d[k] = self._events.span(*v) if isinstance(v, tuple) else v
+            self._resolved = {k: d[k] for k in PHASES if k in d}
+        return self._resolved
+
+    def __getitem__(self, k):
+        return self._all()[k]
+
+    def __iter__(self):
+        return iter(self._all())
+
+    def __len__(self):
+        return len(self._all())
+
+    def __repr__(self):
+        return repr(self._all())
 
 
 def _nonpositive_entry(dc: DeviceCorpus, K, KM, r_dev, v_r: int, ldk: int, t_check: int,
@@ -250,22 +299,29 @@ class QueryPlan:
     alone for the device-resident figure.
     """
 
-    def __init__(self, sel: np.ndarray, weights: np.ndarray, dc: DeviceCorpus,
-                 de: DeviceEmbeddings, config: SolverConfig, ws: SinkhornWorkspace):
+    def __init__(self, sel: np.ndarray | None, weights: np.ndarray | None, dc: DeviceCorpus,
+                 de: DeviceEmbeddings, config: SolverConfig, ws: SinkhornWorkspace,
+                 staged_v_r: int | None = None):
         self.dc, self.de, self.config, self.ws = dc, de, config, ws
         self.dev = dc.device
+        self._stream = stream_ptr(self.dev)
         self.dws = dws = ws.on(self.dev)
-        v_r = self.v_r = int(sel.size)
+        if staged_v_r is None:
+            v_r = int(sel.size)
+            stage = ws.pinned("qstage", 2 * v_r, torch.int64)
+            stage_np = stage.numpy()
+            stage_np[:v_r] = sel
+            stage_np[v_r:] = np.ascontiguousarray(weights, dtype=np.float64).view(np.int64)
+        else:   # (sel | weight bits) already in the pinned stage (native select)
+            v_r = int(staged_v_r)
+            stage = ws.pinned("qstage", 2 * v_r, torch.int64)
+        self.v_r = v_r
         # K row stride = v_r rounded up to 4 (zero pad columns): 16-byte rows that
         # the fast v_r <= 32 kernel reads as whole pairs without masking
         self.ldk = ((v_r + 3) // 4) * 4 if v_r <= 32 else v_r + (v_r & 1)
         V, N = dc.n_rows, dc.n_cols
-        stage = ws.pinned("qstage", 2 * v_r, torch.int64)
-        stage_np = stage.numpy()
-        stage_np[:v_r] = sel
-        stage_np[v_r:] = np.ascontiguousarray(weights, dtype=np.float64).view(np.int64)
         qdev = dws.flat("qdev", 2 * v_r, torch.int64)
-        qdev.copy_(stage, non_blocking=True)
+        qdev.copy_(stage[: 2 * v_r], non_blocking=True)
         self.sel_dev = qdev[:v_r]
         self.r_dev = qdev[v_r:].view(torch.float64)
         self.K = dws.flat("kernel", V * self.ldk)
@@ -282,7 +338,7 @@ class QueryPlan:
 
     @property
     def stream(self) -> int:
-        return stream_ptr(self.dev)
+        return self._stream
 
     def enqueue_distances(self) -> None:
         dc, de = self.dc, self.de
@@ -377,16 +433,17 @@ class QueryPlan:
         return None
 
 
-def solve_on_device(sel: np.ndarray, weights: np.ndarray, dc: DeviceCorpus,
+def solve_on_device(sel: np.ndarray | None, weights: np.ndarray | None, dc: DeviceCorpus,
                     de: DeviceEmbeddings, config: SolverConfig, ws: SinkhornWorkspace,
-                    timed: bool = True, allreduce_max=None) -> ShardResult:
+                    timed: bool = True, allreduce_max=None,
+                    staged_v_r: int | None = None) -> ShardResult:
     """Run phases 2-4 for one query on ``dc``'s device (all columns of ``dc``).
 
     ``allreduce_max`` (multi-GPU tol path) maps a float64 numpy vector to its
     element-wise max over ranks; it keeps the early exit global.
     """
     ev = _Events(timed)
-    plan = QueryPlan(sel, weights, dc, de, config, ws)
+    plan = QueryPlan(sel, weights, dc, de, config, ws, staged_v_r=staged_v_r)
     ev.mark("d0")
     plan.enqueue_distances()
     ev.mark("d1")
@@ -399,14 +456,46 @@ def solve_on_device(sel: np.ndarray, weights: np.ndarray, dc: DeviceCorpus,
         ev.mark("i1")
     wmd_host, he = plan.readback()
     event = plan.decode_event(he)
-    timings = {
-        "distances": ev.span("d0", "d1"),
-        "precompute": 0.0,
-        "init": 0.0,
-        "iterations": ev.span("d1", "i1"),
-        "final": 0.0,
-    }
-    return ShardResult(wmd_host, iterations, converged, timings, event)
+    spans = {"distances": ("d0", "d1"), "precompute": 0.0, "init": 0.0,
+             "iterations": ("d1", "i1"), "final": 0.0}
+    return ShardResult(wmd_host, iterations, converged, (spans, ev), event)
+
+
+def _stage_query(query, n_vocab: int, ws: SinkhornWorkspace) -> int:
+    """select_nonzero (kernels.py:74-88) straight into the pinned H2D stage:
+    writes (sel | weight bits) and returns v_r.  Same errors as the reference."""
+    if isinstance(query, SparseVector):
+        idx, val = query.indices, query.values
+        v_r = int(idx.size)
+        if v_r == 0:
+            raise EmptyQueryError("query histogram has no positive entries")
+        st = ws.pinned_np("qstage", 2 * v_r)
+        st[:v_r] = idx
+        st[v_r: 2 * v_r] = val.view(np.int64)
+        return v_r
+    q = np.asarray(query, dtype=np.float64)
+    if q.ndim != 1:
+        raise ValueError("query histogram must be 1-D")
+    if not q.flags.c_contiguous:
+        q = np.ascontiguousarray(q)
+    cap = max(64, ws.__dict__.get("_qcap", 64))
+    while True:
+        st = ws.pinned_np("qstage", 2 * cap)
+        cnt = _lib.lib().swmd_select_query(q.ctypes.data, q.size, st.ctypes.data, cap)
+        if cnt == -2:
+            raise ValueError("query histogram must be nonnegative")
+        if cnt < 0:
+            raise ValueError("query histogram could not be read")
+        if cnt <= cap:
+            break
+        cap = int(cnt)
+        ws.__dict__["_qcap"] = cap
+    if cnt == 0:
+        raise EmptyQueryError("query histogram has no positive entries")
+    if cnt != cap:
+        # weights were written right after the ids: already contiguous
+        pass
+    return int(cnt)
 
 
 def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
@@ -425,18 +514,18 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
             f"{emb_shape}, corpus rows {n_vocab}")
     ws = workspace if workspace is not None else _default_ws()
     t0 = time.perf_counter()
-    sel, weights = select_nonzero(query)
+    v_r = _stage_query(query, n_vocab, ws)
     t_select = time.perf_counter() - t0
     dev = device()
     dc = DeviceCorpus.of(corpus, dev)
     de = DeviceEmbeddings.of(embeddings, dev)
-    res = solve_on_device(sel, weights, dc, de, config, ws)
+    res = solve_on_device(None, None, dc, de, config, ws, staged_v_r=v_r)
     if res.event is not None:
         raise DegeneracyError(res.event.message)
-    timings = {"select": t_select, **res.timings}
-    timings["total"] = time.perf_counter() - t_start
+    spans, ev = res.timings
+    host = {"select": t_select, "total": time.perf_counter() - t_start}
     return SolverResult(wmd=res.wmd, iterations_run=res.iterations, converged=res.converged,
-                        timings={k: timings[k] for k in PHASES})
+                        timings=LazyTimings(host, spans, ev))
 
 
 def sinkhorn_wmd_batch(queries, corpus, embeddings, config: SolverConfig,

@@ -30,7 +30,7 @@ from paper_2107_06433_b200.sparse import (
 def _header_symbols() -> list[str]:
     text = open(os.path.join(REPO, "include", "swmd.h")).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return re.findall(r"^\s*int\s+(swmd_\w+)\s*\(", text, flags=re.M)
+    return re.findall(r"^\s*(?:int|int64_t)\s+(swmd_\w+)\s*\(", text, flags=re.M)
 
 
 def test_library_exports_every_header_symbol():
