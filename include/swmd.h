@@ -172,6 +172,31 @@ int swmd_update_u_f64(const double* x, double* u, int64_t n, int32_t code,
  * entry (EmptyQueryError). */
 int64_t swmd_select_query(const double* r, int64_t n, int64_t* stage, int64_t cap);
 
+/*
+ * Native per-query runtime (replaces the Python orchestration of
+ * solver.py:106-201 for the common case tol == NULL, v_r <= 32).
+ * swmd_plan_create binds the resident buffers once; desc is an int64 array:
+ *   [0] E  [1] V  [2] dim  [3] ldE  [4] norms  [5] col_ptr  [6] rows  [7] vals
+ *   [8] n_cols  [9] order  [10] present rows (or 0)  [11] n_present
+ *   [12] col_key_offset  [13] n_key  [14] max_len  [15] group_hint
+ *   [16] K  [17] KM  [18] K/KM capacity (doubles)  [19] device stage (2*q_cap
+ *   int64)  [20] pinned host stage (2*q_cap int64)  [21] q_cap
+ *   [22] device out (n_cols doubles + 4 int64)  [23] pinned host out (same)
+ *   [24] int32 counter  [25] stream (optional)
+ * swmd_plan_run: select (host) -> H2D -> cost build -> solve -> D2H -> sync;
+ * copies the distances to wmd_host and the error record to err_host and the
+ * cost / solve device times (ms) to times_ms[0..1] and the host select time
+ * (ms) to times_ms[2].  Returns 0, a CUDA
+ * error, -2 (negative query entry), -3 (no positive entry) or -4 (query
+ * outside the plan's fast path: the caller uses the general entry points).
+ */
+typedef struct swmd_plan swmd_plan;
+int swmd_plan_create(swmd_plan** out, const int64_t* desc, int32_t n);
+int swmd_plan_destroy(swmd_plan* plan);
+int swmd_plan_run(swmd_plan* plan, const double* query, int64_t V, double lam,
+                  int32_t max_iter, int32_t cost_mode, double* wmd_host,
+                  int64_t* err_host, float* times_ms, int64_t* v_r_out);
+
 /* Flush helper for benchmarks: writes `bytes` of scratch (> L2 evicts
  * everything) and reads it back, leaving L2 clean (no dirty write-back is
  * charged to the next kernel). */

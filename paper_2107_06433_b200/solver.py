@@ -498,6 +498,71 @@ def _stage_query(query, n_vocab: int, ws: SinkhornWorkspace) -> int:
     return int(cnt)
 
 
+class NativePlan:
+    """The native per-query runtime (swmd_plan_run) bound to one resident
+    corpus and embedding table: buffers owned here, pointers handed to C once."""
+
+    Q_CAP = 32
+
+    def __init__(self, dc: DeviceCorpus, de: DeviceEmbeddings):
+        dev = dc.device
+        self.dc, self.de = dc, de
+        V, N = dc.n_rows, dc.n_cols
+        self.K = torch.empty(V * 32, dtype=torch.float64, device=dev)
+        self.KM = torch.empty(V * 32, dtype=torch.float64, device=dev)
+        self.qdev = torch.empty(2 * self.Q_CAP, dtype=torch.int64, device=dev)
+        self.qhost = torch.empty(2 * self.Q_CAP, dtype=torch.int64, pin_memory=True)
+        self.out_dev = torch.empty(N + _lib.ERR_WORDS, dtype=torch.int64, device=dev)
+        self.out_host = torch.empty(N + _lib.ERR_WORDS, dtype=torch.int64, pin_memory=True)
+        self.counter = torch.empty(1, dtype=torch.int32, device=dev)
+        self.err = np.empty(_lib.ERR_WORDS, dtype=np.int64)
+        self.times = np.zeros(3, dtype=np.float32)
+        self.vr = np.zeros(1, dtype=np.int64)
+        norms = de.norms
+        pres = dc.present_rows
+        desc = np.array([
+            de.E.data_ptr(), de.V, de.dim, de.ld, norms.data_ptr(),
+            dc.col_ptr.data_ptr(), dc.rows.data_ptr(), dc.vals.data_ptr(), N,
+            dc.order.data_ptr(), pres.data_ptr() if pres is not None else 0, dc.n_present,
+            dc.col_offset, dc.n_key, dc.max_len, _group(dc, 19),
+            self.K.data_ptr(), self.KM.data_ptr(), V * 32,
+            self.qdev.data_ptr(), self.qhost.data_ptr(), self.Q_CAP,
+            self.out_dev.data_ptr(), self.out_host.data_ptr(), self.counter.data_ptr(),
+            stream_ptr(dev)], dtype=np.int64)
+        import ctypes
+        h = ctypes.c_void_p()
+        _lib.call("swmd_plan_create", ctypes.byref(h), desc.ctypes.data, desc.size)
+        self.handle = h
+        self._args = (self.err.ctypes.data, self.times.ctypes.data, self.vr.ctypes.data)
+        self._stream = stream_ptr(dev)
+
+    def __del__(self):
+        try:
+            _lib.lib().swmd_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+    def run(self, q: np.ndarray, config: SolverConfig):
+        """Returns (rc, wmd).  rc: 0 ok, -2/-3 argument errors, -4 general path."""
+        wmd = np.empty(self.dc.n_cols, dtype=np.float64)
+        mode = COST_MODE_GRAM if config.cost_mode == "gram" else COST_MODE_DIRECT
+        rc = _lib.lib().swmd_plan_run(self.handle, q.ctypes.data, q.size, float(config.lam),
+                                      int(config.max_iter), mode, wmd.ctypes.data, *self._args)
+        return rc, wmd
+
+
+def _native_plan(ws: SinkhornWorkspace, dc: DeviceCorpus, de: DeviceEmbeddings,
+                 dev: torch.device) -> "NativePlan | None":
+    key = (id(dc), id(de))
+    cache = ws.__dict__.setdefault("_native_plans", {})
+    plan = cache.get(key)
+    if plan is None or plan.dc is not dc or plan.de is not de or plan._stream != stream_ptr(dev):
+        plan = NativePlan(dc, de)
+        cache.clear()          # one resident plan per workspace
+        cache[key] = plan
+    return plan
+
+
 def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
                  workspace: SinkhornWorkspace | None = None) -> SolverResult:
     """Regularised transport distance of one query to every corpus column
@@ -513,6 +578,30 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
             f"shape mismatch: query {query.shape}, embeddings "
             f"{emb_shape}, corpus rows {n_vocab}")
     ws = workspace if workspace is not None else _default_ws()
+    if (config.tol is None and isinstance(query, np.ndarray) and query.dtype == np.float64
+            and query.ndim == 1 and query.flags.c_contiguous and corpus.n_cols > 0
+            and torch.cuda.is_available()):
+        # native runtime: one C call does select -> H2D -> kernels -> D2H
+        dev = device()
+        dc = DeviceCorpus.of(corpus, dev)
+        de = DeviceEmbeddings.of(embeddings, dev)
+        plan = _native_plan(ws, dc, de, dev)
+        rc, wmd = plan.run(query, config)
+        if rc == -2:
+            raise ValueError("query histogram must be nonnegative")
+        if rc == -3:
+            raise EmptyQueryError("query histogram has no positive entries")
+        if rc > 0:
+            raise _lib.NativeError(f"swmd_plan_run: CUDA error {rc}")
+        if rc == 0 and plan.err[0] == _lib.NO_EVENT and plan.err[1] == _lib.NO_EVENT:
+            t = plan.times
+            timings = {"select": float(t[2]) / 1e3, "distances": float(t[0]) / 1e3,
+                       "precompute": 0.0, "init": 0.0, "iterations": float(t[1]) / 1e3,
+                       "final": 0.0, "total": time.perf_counter() - t_start}
+            return SolverResult(wmd=wmd, iterations_run=config.max_iter, converged=False,
+                                timings=timings)
+        # rc == -4 (outside the native fast path) or a degeneracy to decode:
+        # the general path below reproduces the reference's error exactly
     t0 = time.perf_counter()
     v_r = _stage_query(query, n_vocab, ws)
     t_select = time.perf_counter() - t0
