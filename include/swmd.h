@@ -120,6 +120,29 @@ int swmd_solve_f64(const int64_t* col_ptr, const int32_t* rows, const double* va
                    int32_t max_len_hint, int64_t* err, int32_t* counter, void* stream);
 
 /*
+ * fp32 multi-query variant (BASELINE config c4; the reference is fp64-only,
+ * so these twin the f64 entry points for a batch of queries).
+ * swmd_cost_build_batch_f32: one GEMM over the concatenated words of a batch;
+ * output column c (of LD, LD % 4 == 0) holds word words[col_word[c]]
+ * (col_word[c] == -1: zero padding).  K, K*M are (V, LD) fp32.
+ * swmd_solve_f32: swmd_solve_f64 on fp32 K / K*M / weights / x / wmd; a
+ * query's K block starts at its first column (16-byte aligned) with row
+ * stride ldk = LD and zero padding up to v_r rounded to 8.
+ */
+int swmd_row_norms_f32(const float* E, int64_t V, int32_t dim, int64_t ldE, float* norms,
+                       void* stream);
+int swmd_cost_build_batch_f32(const float* E, int64_t V, int32_t dim, int64_t ldE,
+                              const int64_t* words, const int32_t* col_word, int32_t LD,
+                              float lam, const float* norms, const int32_t* row_list,
+                              int64_t n_list, float* kernel, float* kernel_cost, void* stream);
+int swmd_solve_f32(const int64_t* col_ptr, const int32_t* rows, const double* vals,
+                   int64_t n_cols, const int32_t* order, const float* kernel,
+                   const float* kernel_cost, const float* weights, int32_t v_r, int64_t ldk,
+                   int32_t t_begin, int32_t t_end, const float* x_in, float* x_out, float* wmd,
+                   int64_t col_key_offset, int64_t n_key, int32_t max_len_hint, int64_t* err,
+                   int32_t* counter, void* stream);
+
+/*
  * One fused type-1 iteration with explicit u and kernel_over_r, accumulating
  * into x (x[j,a] += sum ...; zero it first for a fresh iteration):
  * replaces _jit.fused_iter_serial / _columns (_jit.py:120-137, 164-183) as

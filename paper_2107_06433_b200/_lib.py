@@ -55,6 +55,11 @@ _SIGS = {
     "swmd_update_u_f64": [_P, _P, _I64, _I32, _P, _P],
     "swmd_l2_flush": [_P, _I64, _P],
     "swmd_select_query": [_P, _I64, _P, _I64],
+    "swmd_row_norms_f32": [_P, _I64, _I32, _I64, _P, _P],
+    "swmd_cost_build_batch_f32": [_P, _I64, _I32, _I64, _P, _P, _I32, ctypes.c_float, _P, _P,
+                                  _I64, _P, _P, _P],
+    "swmd_solve_f32": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
+                       _I64, _I64, _I32, _P, _P, _P],
     "swmd_plan_create": [_P, _P, _I32],
     "swmd_plan_destroy": [_P],
     "swmd_plan_run": [_P, _P, _I64, _D, _I32, _I32, _P, _P, _P, _P],

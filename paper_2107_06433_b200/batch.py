@@ -1,0 +1,204 @@
+"""Multi-query fp32 variant: a whole batch of queries in one cost-build launch.
+
+BASELINE config c4 (64 queries, v_r in [8, 64], N=100k documents, fp32,
+max_iter=20, tolerance 1e-4 vs the fp64 oracle).  The reference is fp64-only
+and solves a batch one query at a time (``sinkhorn_wmd_batch``,
+solver.py:204-223); this path keeps its contract — one ``SolverResult`` or
+exception per query, a failing query never aborts the batch — and batches the
+work the B200 way:
+
+* the selected words of every query are concatenated and ONE fp32 GEMM
+  (``swmd_cost_build_batch_f32``) builds K and K*M for all of them, reading
+  the (fp32, resident) embedding table once per 64 output columns;
+* each query's K block is a 16-byte-aligned column range of that matrix,
+  zero-padded to v_r rounded to 8, and the fp32 solve kernel reads it in
+  place (row stride = the batch width);
+* one device->host copy returns every query's distances and error record.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceCorpus, DeviceEmbeddings, device, stream_ptr
+from .kernels import DegeneracyError, select_nonzero, zero_denominator_event
+from .sparse import SparseVector
+
+__all__ = ["solve_batch_f32"]
+
+_INT64_MAX = (1 << 63) - 1
+
+
+def _block_width(v_r: int) -> int:
+    return (v_r + 7) // 8 * 8 if v_r <= 64 else (v_r + 3) // 4 * 4
+
+
+def _solve32(dc, K_ptr, KM_ptr, r_ptr, v_r, LD, t0, t1, x_in, x_out, wmd_ptr, err_ptr, counter, s):
+    _lib.call("swmd_solve_f32", dc.col_ptr.data_ptr(), dc.rows.data_ptr(), dc.vals.data_ptr(),
+              dc.n_cols, dc.order.data_ptr(), K_ptr, KM_ptr, r_ptr, v_r, LD, t0, t1,
+              x_in, x_out, wmd_ptr, dc.col_offset, dc.n_key, dc.max_len, err_ptr,
+              counter.data_ptr(), s)
+
+
+def _reset_err(err: torch.Tensor) -> None:
+    e = err.view(-1, _lib.ERR_WORDS)
+    e[:, 0] = _INT64_MAX
+    e[:, 1] = _INT64_MAX
+    e[:, 2] = 0
+    e[:, 3] = _INT64_MAX
+
+
+def solve_batch_f32(queries, corpus, embeddings, config, ws) -> list:
+    """``sinkhorn_wmd_batch`` semantics in fp32 (see module docstring)."""
+    from .solver import SolverResult
+
+    t_start = time.perf_counter()
+    n_vocab = corpus.n_rows
+    emb_shape = tuple(embeddings.shape)
+    results: list = [None] * len(queries)
+    items = []
+    t0 = time.perf_counter()
+    for k, q in enumerate(queries):
+        try:
+            if isinstance(q, SparseVector):
+                q = q.to_dense()
+            q = np.asarray(q, dtype=np.float64)
+            if q.shape != (n_vocab,) or emb_shape[0] != n_vocab:
+                raise ValueError(f"shape mismatch: query {q.shape}, embeddings {emb_shape}, "
+                                 f"corpus rows {n_vocab}")
+            sel, w = select_nonzero(q)
+            items.append((k, sel, w))
+        except (ValueError, ArithmeticError) as exc:
+            results[k] = exc
+    t_select = time.perf_counter() - t0
+    if not items:
+        return results
+
+    dev = device()
+    s = stream_ptr(dev)
+    dc = DeviceCorpus.of(corpus, dev)
+    de = DeviceEmbeddings.of(embeddings, dev, dtype=torch.float32)
+    dws = ws.on(dev)
+    V, N = dc.n_rows, dc.n_cols
+    # column layout of the batch
+    offs, woffs, off, woff = [], [], 0, 0
+    for _, sel, _ in items:
+        offs.append(off)
+        woffs.append(woff)
+        off += _block_width(sel.size)
+        woff += sel.size
+    LD = (off + 3) // 4 * 4
+    words = np.concatenate([sel for _, sel, _ in items]).astype(np.int64)
+    weights = np.concatenate([w for _, _, w in items]).astype(np.float32)
+    col_word = np.full(LD, -1, dtype=np.int32)
+    for (_, sel, _), o, wo in zip(items, offs, woffs):
+        col_word[o: o + sel.size] = np.arange(wo, wo + sel.size, dtype=np.int32)
+    words_d = torch.from_numpy(words).to(dev, non_blocking=True)
+    col_d = torch.from_numpy(col_word).to(dev, non_blocking=True)
+    w_d = torch.from_numpy(weights).to(dev, non_blocking=True)
+
+    K = dws.flat("k32", V * LD, torch.float32)
+    KM = dws.flat("km32", V * LD, torch.float32)
+    use_list = dc.present_rows is not None and dc.n_present < V
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    _lib.call("swmd_cost_build_batch_f32", de.E.data_ptr(), de.V, de.dim, de.ld,
+              words_d.data_ptr(), col_d.data_ptr(), LD, float(config.lam), de.norms.data_ptr(),
+              dc.present_rows.data_ptr() if use_list else None,
+              dc.n_present if use_list else 0, K.data_ptr(), KM.data_ptr(), s)
+    ev[1].record()
+
+    nq = len(items)
+    out = dws.flat("wmd32", nq * N, torch.float32)
+    err = dws.flat("err32", nq * _lib.ERR_WORDS, torch.int64)
+    counter = dws.flat("counter32", 1, torch.int32)
+    _reset_err(err)
+    iters = [config.max_iter] * nq
+    conv = [False] * nq
+    for n, ((k, sel, _), o, wo) in enumerate(zip(items, offs, woffs)):
+        Kp = K.data_ptr() + 4 * o
+        KMp = KM.data_ptr() + 4 * o
+        rp = w_d.data_ptr() + 4 * wo
+        wmd_p = out.data_ptr() + 4 * n * N
+        err_p = err.data_ptr() + 8 * n * _lib.ERR_WORDS
+        if config.tol is None:
+            _solve32(dc, Kp, KMp, rp, sel.size, LD, 0, config.max_iter, None, None, wmd_p,
+                     err_p, counter, s)
+        else:
+            iters[n], conv[n] = _tol_loop(dc, Kp, KMp, rp, sel.size, LD, wmd_p, err, n,
+                                          counter, s, config, dws)
+    ev[2].record()
+    wmd_h = out.view(nq, N).cpu().numpy()
+    err_h = err.view(nq, _lib.ERR_WORDS).cpu().numpy()
+    t_dist = ev[0].elapsed_time(ev[1]) / 1e3
+    t_iter = ev[1].elapsed_time(ev[2]) / 1e3
+    t_total = time.perf_counter() - t_start
+    for n, ((k, sel, _), o, wo) in enumerate(zip(items, offs, woffs)):
+        msg = _error_message(err_h[n], dc, K.data_ptr() + 4 * o, KM.data_ptr() + 4 * o,
+                             w_d.data_ptr() + 4 * wo, sel.size, LD, counter, s, dws)
+        if msg is not None:
+            results[k] = DegeneracyError(msg)
+            continue
+        timings = {"select": t_select / nq, "distances": t_dist / nq, "precompute": 0.0,
+                   "init": 0.0, "iterations": t_iter / nq, "final": 0.0, "total": t_total / nq}
+        results[k] = SolverResult(wmd=wmd_h[n].astype(np.float64), iterations_run=iters[n],
+                                  converged=conv[n], timings=timings)
+    return results
+
+
+def _tol_loop(dc, Kp, KMp, rp, v_r, LD, wmd_p, err, n, counter, s, config, dws):
+    """Per-iteration launches with the max-norm change read back (solver.py:170-183)."""
+    N = dc.n_cols
+    bufs = (dws.flat("x32a", N * v_r, torch.float32), dws.flat("x32b", N * v_r, torch.float32))
+    e = err.view(-1, _lib.ERR_WORDS)[n]
+    err_p = e.data_ptr()
+    cur, iterations, converged = None, 0, False
+    for t in range(config.max_iter):
+        nxt = bufs[t % 2]
+        e[2] = 0
+        _solve32(dc, Kp, KMp, rp, v_r, LD, t, t + 1, cur.data_ptr() if cur is not None else None,
+                 nxt.data_ptr(), None, err_p, counter, s)
+        he = e.cpu().numpy()
+        iterations += 1
+        cur = nxt
+        if he[0] != _INT64_MAX or he[1] != _INT64_MAX:
+            return iterations, False
+        if float(he[2:3].view(np.float64)[0]) < config.tol:
+            converged = True
+            break
+    _solve32(dc, Kp, KMp, rp, v_r, LD, iterations, iterations, cur.data_ptr(), None, wmd_p,
+             err_p, counter, s)
+    return iterations, converged
+
+
+def _error_message(he, dc, Kp, KMp, rp, v_r, LD, counter, s, dws):
+    zd = zero_denominator_event(he, dc.n_key)
+    code_zero = zd[0] if zd is not None else None
+    code_np = int(he[1]) if he[1] != _INT64_MAX else None
+    code_nan = int(he[3]) if he[3] != _INT64_MAX else None
+    if code_np is not None and code_nan is not None and code_nan <= code_np:
+        code_np = None
+    if code_np is not None and (code_zero is None or code_np < code_zero):
+        # replay to the failing check with x stored (rare error path)
+        N = dc.n_cols
+        xa = dws.flat("x32ra", N * v_r, torch.float32)
+        xb = dws.flat("x32rb", N * v_r, torch.float32)
+        e = torch.empty(_lib.ERR_WORDS, dtype=torch.int64, device=dc.device)
+        cur = None
+        for t in range(code_np // 2):
+            nxt = (xa, xb)[t % 2]
+            _reset_err(e)
+            _solve32(dc, Kp, KMp, rp, v_r, LD, t, t + 1,
+                     cur.data_ptr() if cur is not None else None, nxt.data_ptr(), None,
+                     e.data_ptr(), counter, s)
+            cur = nxt
+        flat_local = int(torch.argmin(cur).item())
+        val = float(cur[flat_local].item())
+        return f"nonpositive iterate entry {val} at flat index {dc.col_offset * v_r + flat_local}"
+    if zd is not None:
+        return f"zero denominator at nonzero ({zd[1]}, {zd[2]})"
+    return None

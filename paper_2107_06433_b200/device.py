@@ -135,54 +135,73 @@ def _fingerprint(a: np.ndarray) -> int:
 
 
 class DeviceEmbeddings:
-    """An embedding table resident in HBM (f64, row-major) with its row norms."""
+    """An embedding table resident in HBM, row-major, with its row norms.
+
+    float64 for the reference-precision path; float32 (rows padded to a
+    multiple of 4 elements, 16-byte aligned) for the multi-query fp32 path.
+    """
 
     _cache: dict = {}
 
-    def __init__(self, E: torch.Tensor):
+    def __init__(self, E: torch.Tensor, dim: int | None = None):
         self.E = E
-        self.V, self.dim = int(E.shape[0]), int(E.shape[1])
+        self.V = int(E.shape[0])
+        self.dim = int(dim if dim is not None else E.shape[1])
         self.ld = int(E.stride(0))
+        self.dtype = E.dtype
         self._norms = None
 
     @property
     def norms(self) -> torch.Tensor:
         if self._norms is None:
-            n = torch.empty(self.V, dtype=torch.float64, device=self.E.device)
-            _lib.call("swmd_row_norms_f64", self.E.data_ptr(), self.V, self.dim, self.ld,
-                      n.data_ptr(), stream_ptr(self.E.device))
+            n = torch.empty(self.V, dtype=self.dtype, device=self.E.device)
+            fn = "swmd_row_norms_f64" if self.dtype == torch.float64 else "swmd_row_norms_f32"
+            _lib.call(fn, self.E.data_ptr(), self.V, self.dim, self.ld, n.data_ptr(),
+                      stream_ptr(self.E.device))
             self._norms = n
         return self._norms
 
     @classmethod
-    def of(cls, E, dev: torch.device | None = None) -> "DeviceEmbeddings":
+    def of(cls, E, dev: torch.device | None = None,
+           dtype: torch.dtype = torch.float64) -> "DeviceEmbeddings":
         if isinstance(E, torch.Tensor):
             if E.device.type != "cuda":
                 E = E.detach().cpu().numpy()
-            else:
+            elif dtype == torch.float64:
                 t = E.detach()
                 if t.dtype != torch.float64:
                     t = t.double()
                 if t.stride(-1) != 1:
                     t = t.contiguous()
-                key = ("torch", t.data_ptr(), tuple(t.shape), t._version)
+                key = ("torch", t.data_ptr(), tuple(t.shape), t._version, dtype)
                 de = cls._cache.get(key)
                 if de is None:
                     de = cls(t)
-                    cls._cache = {key: de}
+                    cls._cache = {k: v for k, v in cls._cache.items() if k[0] != "torch"}
+                    cls._cache[key] = de
                 return de
+            else:
+                E = E.detach().cpu().numpy()
         dev = dev or device()
         arr = np.asarray(E)
         if arr.ndim != 2:
             raise ValueError(f"embeddings must be 2-D, got shape {arr.shape}")
         key = ("numpy", dev.index, arr.__array_interface__["data"][0], arr.shape,
-               arr.strides, arr.dtype.str, _fingerprint(arr))
+               arr.strides, arr.dtype.str, _fingerprint(arr), dtype)
         de = cls._cache.get(key)
         if de is None:
-            host = np.ascontiguousarray(arr, dtype=np.float64)
-            de = cls(_h2d(host, dev))
-            # keep one resident table per device (a new one evicts the old)
-            cls._cache = {k: v for k, v in cls._cache.items() if k[0] == "torch"}
+            if dtype == torch.float64:
+                host = np.ascontiguousarray(arr, dtype=np.float64)
+                de = cls(_h2d(host, dev))
+            else:
+                V, dim = arr.shape
+                ld = (dim + 3) // 4 * 4
+                host = np.zeros((V, ld), dtype=np.float32)
+                host[:, :dim] = arr
+                de = cls(_h2d(host, dev), dim=dim)
+            # keep one resident table per (device, precision): a new one evicts the old
+            cls._cache = {k: v for k, v in cls._cache.items()
+                          if k[0] == "torch" or k[-1] != dtype}
             cls._cache[key] = de
         return de
 

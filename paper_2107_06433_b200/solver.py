@@ -69,6 +69,9 @@ class SolverConfig:
     ``cost_mode`` selects the distance form: "gram" (default; fused
     ||e||^2+||q||^2-2e.q with an exact zero self-distance) or "direct" (the
     reference's difference form, bitwise-identical distances).
+    ``precision="f32"`` selects the multi-query fp32 variant (BASELINE c4;
+    batch.py): fp32 embeddings, kernel matrices and iterates, results within
+    1e-4 of the fp64 reference.
     """
 
     lam: float = 10.0
@@ -77,6 +80,7 @@ class SolverConfig:
     workers: int = 1
     deterministic: bool = False
     cost_mode: str = "gram"
+    precision: str = "f64"
 
     def __post_init__(self):
         if self.lam <= 0.0:
@@ -89,6 +93,8 @@ class SolverConfig:
             raise ValueError(f"tol must be nonnegative, got {self.tol}")
         if self.cost_mode not in ("gram", "direct"):
             raise ValueError(f"cost_mode must be 'gram' or 'direct', got {self.cost_mode!r}")
+        if self.precision not in ("f64", "f32"):
+            raise ValueError(f"precision must be 'f64' or 'f32', got {self.precision!r}")
 
 
 @dataclass(frozen=True)
@@ -578,6 +584,13 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
             f"shape mismatch: query {query.shape}, embeddings "
             f"{emb_shape}, corpus rows {n_vocab}")
     ws = workspace if workspace is not None else _default_ws()
+    if config.precision == "f32":
+        from .batch import solve_batch_f32
+
+        res = solve_batch_f32([query], corpus, embeddings, config, ws)[0]
+        if isinstance(res, Exception):
+            raise res
+        return res
     if (config.tol is None and isinstance(query, np.ndarray) and query.dtype == np.float64
             and query.ndim == 1 and query.flags.c_contiguous and corpus.n_cols > 0
             and torch.cuda.is_available()):
@@ -622,6 +635,10 @@ def sinkhorn_wmd_batch(queries, corpus, embeddings, config: SolverConfig,
     """Independent solves sharing one workspace; a failing query yields its
     exception instead of aborting the batch (solver.py:204-223)."""
     ws = workspace if workspace is not None else SinkhornWorkspace()
+    if config.precision == "f32":
+        from .batch import solve_batch_f32
+
+        return solve_batch_f32(list(queries), corpus, embeddings, config, ws)
     results: list = []
     for q in queries:
         try:

@@ -133,12 +133,47 @@ def make_config(name: str, full: bool):
           f"solve {t3 - t2:.2f}s timings {res.timings}")
 
 
+def make_c4():
+    """64 fp64 reference solves on the c4 instance (the fp32 path is checked
+    against these within 1e-4)."""
+    cfg = synth.CONFIGS["c4"]
+    t0 = time.time()
+    inst = synth.zipf_instance(cfg)
+    rp, ci, v = synth.csc_to_csr(inst.n_vocab, inst.n_docs, inst.col_ptr, inst.rows, inst.vals)
+    corpus = CsrMatrix(inst.n_vocab, inst.n_docs, rp, ci, v)
+    corpus.csc_index()
+    scfg = sinkwmd.SolverConfig(lam=cfg.lam, max_iter=cfg.max_iter,
+                                workers=os.cpu_count() or 1, deterministic=True)
+    E64 = inst.embeddings.astype(np.float64)
+    stride = max(1, inst.n_docs // 500)
+    tops, topv, sums, samples, vrs = [], [], [], [], []
+    for q in inst.queries:
+        res = sinkwmd.sinkhorn_wmd(q, corpus, E64, scfg)
+        order = np.argsort(res.wmd, kind="stable")
+        tops.append(order[:10])
+        topv.append(res.wmd[order[:10]])
+        sums.append(float(np.sum(res.wmd)))
+        samples.append(res.wmd[::stride])
+        vrs.append(int(np.count_nonzero(q)))
+    np.savez_compressed(
+        os.path.join(HERE, "c4.npz"), config=np.array("c4"), seed=np.array(cfg.seed),
+        nnz=np.array(inst.nnz),
+        fp_corpus=np.array(fingerprint(inst.col_ptr, inst.rows, inst.vals)),
+        fp_embeddings=np.array(fingerprint(inst.embeddings)),
+        top10=np.array(tops), top10_wmd=np.array(topv), wmd_sum=np.array(sums),
+        sample_stride=np.array(stride), sample=np.array(samples), v_r=np.array(vrs))
+    print(f"c4.npz: nnz={inst.nnz} queries={len(inst.queries)} v_r={vrs[:8]}... "
+          f"{time.time() - t0:.1f}s")
+
+
 def main(argv):
     sinkwmd.kernels.warmup()
-    which = argv or ["small", "c1", "c2", "c3", "c5"]
+    which = argv or ["small", "c1", "c2", "c3", "c4", "c5"]
     for w in which:
         if w == "small":
             make_small()
+        elif w == "c4":
+            make_c4()
         else:
             make_config(w, full=w in ("c1", "c2"))
 

@@ -346,3 +346,55 @@ def test_torch_cuda_embeddings():
     a = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
     b = swmd.sinkhorn_wmd(inst.query, corpus, torch.from_numpy(inst.embeddings).cuda(), cfg).wmd
     assert np.array_equal(a, b)
+
+
+# -- fp32 multi-query variant (BASELINE config c4) ----------------------------------------------
+
+F32_RTOL = 1e-4
+
+
+def test_c4_fp32_batch_matches_fp64_reference():
+    g = golden("c4")
+    inst = synth.zipf_instance("c4")
+    cfg = swmd.SolverConfig(lam=10.0, max_iter=20, precision="f32")
+    res = swmd.sinkhorn_wmd_batch(inst.queries, inst.corpus(), inst.embeddings, cfg)
+    stride = int(g["sample_stride"])
+    worst = 0.0
+    for k, r in enumerate(res):
+        assert isinstance(r, swmd.SolverResult), r
+        worst = max(worst, max_rel_err(r.wmd[::stride], g["sample"][k]))
+        assert abs(float(np.sum(r.wmd)) - float(g["wmd_sum"][k])) <= F32_RTOL * float(g["wmd_sum"][k])
+        top = g["top10"][k]
+        assert max_rel_err(r.wmd[top], g["top10_wmd"][k]) <= F32_RTOL
+        order = np.argsort(r.wmd, kind="stable")[:10]
+        # fp32 may reorder reference near-ties (within the tolerance band)
+        if not np.array_equal(order, top):
+            srt = np.sort(g["top10_wmd"][k])
+            gaps = np.diff(srt) / srt[1:]
+            assert np.min(gaps) <= 2 * F32_RTOL, (k, order, top)
+    assert worst <= F32_RTOL, worst
+
+
+def test_fp32_batch_contract(oracle_lib):
+    rng = np.random.default_rng(44)
+    V, N = 3000, 120
+    emb = synth.normal_embeddings(rng, V, 64, np.float32)
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, 5, 40)
+    corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+    queries = [synth.zipf_query(rng, V, v) for v in (3, 8, 19, 64, 100)]
+    queries.insert(2, np.zeros(V))                  # fails alone, batch continues
+    cfg = swmd.SolverConfig(lam=10.0, max_iter=15, precision="f32")
+    out = swmd.sinkhorn_wmd_batch(queries, corpus, emb, cfg)
+    assert isinstance(out[2], swmd.EmptyQueryError)
+    for q, r in zip(queries, out):
+        if isinstance(r, Exception):
+            continue
+        want = oracle_lib.solve(q, cp, rows, vals, emb.astype(np.float64), lam=10.0,
+                                max_iter=15).wmd
+        assert max_rel_err(r.wmd, want) <= F32_RTOL
+    # single-query entry point and the tol path in fp32
+    one = swmd.sinkhorn_wmd(queries[3], corpus, emb, cfg)
+    assert np.array_equal(one.wmd, out[3].wmd)
+    tol = swmd.sinkhorn_wmd(queries[3], corpus, emb,
+                            swmd.SolverConfig(lam=1.0, max_iter=300, tol=1e-6, precision="f32"))
+    assert tol.converged and tol.iterations_run < 300

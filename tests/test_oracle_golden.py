@@ -98,3 +98,15 @@ def test_column_blocks_match_reference_semantics(oracle_lib):
         cp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
         for p in (1, 2, 3, 5, 8, 64):
             assert np.array_equal(oracle_lib.column_blocks(cp, p), column_blocks(cp, p))
+
+
+def test_c4_oracle_pinned_on_four_queries(oracle_lib):
+    g = golden("c4")
+    inst = synth.zipf_instance("c4")
+    assert _fp(inst.col_ptr, inst.rows, inst.vals) == str(g["fp_corpus"])
+    E64 = inst.embeddings.astype(np.float64)
+    stride = int(g["sample_stride"])
+    for k in (0, 21, 42, 63):
+        res = oracle_lib.solve(inst.queries[k], inst.col_ptr, inst.rows, inst.vals, E64,
+                               lam=10.0, max_iter=20)
+        assert np.array_equal(res.wmd[::stride], g["sample"][k]), k
