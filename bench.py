@@ -331,7 +331,7 @@ def run_b200(args):
             ncu = json.load(f)["kernels"]
     except (OSError, KeyError, ValueError):
         pass
-    kname = "hybrid_solve" if dominant == "solve" else "cost_dmma_kernel"
+    kname = "hybrid_solve" if dominant == "solve" else "cost_tmap_kernel"
     traffic = None
     if kname in ncu and args.config == "c2" and world == 1:
         traffic = ncu[kname]["dram_read_bytes"] + ncu[kname]["dram_write_bytes"]

@@ -84,6 +84,20 @@ int swmd_cost_build_f64(const double* E, int64_t V, int32_t dim, int64_t ldE,
                         double* cost, double* kernel, double* kernel_over_r,
                         double* kernel_cost, int64_t ldk, void* stream);
 
+/*
+ * swmd_cost_build_f64 (Gram mode) for the rows a corpus actually uses, read
+ * from their compacted copy E_c (n_c x dim, row stride ldEc, dim and ldEc
+ * even): row r of E_c is vocabulary row row_ids[r] (row_ids NULL: identity).
+ * E (row stride ldE) supplies the query vectors, norms are per vocabulary row.
+ * Streams E_c through TMA tensor copies (cp.async.bulk.tensor, 128-byte
+ * swizzle, 16-stage mbarrier ring) into the FP64 tensor pipe (DMMA).
+ */
+int swmd_cost_build_compact_f64(const double* E, int64_t ldE, const double* E_c, int64_t n_c,
+                                int32_t dim, int64_t ldEc, const int32_t* row_ids,
+                                const int64_t* sel, int32_t v_r, const double* weights,
+                                double lam, const double* norms, double* kernel,
+                                double* kernel_cost, int64_t ldk, void* stream);
+
 /* Elementwise precompute from a given cost matrix: replaces
  * _jit.precompute_mats (_jit.py:105-114) behind kernels.precompute
  * (kernels.py:114-141).  kernel_over_r / kernel_cost may be NULL. */
@@ -205,7 +219,8 @@ int64_t swmd_select_query(const double* r, int64_t n, int64_t* stage, int64_t ca
  *   [16] K  [17] KM  [18] K/KM capacity (doubles)  [19] device stage (2*q_cap
  *   int64)  [20] pinned host stage (2*q_cap int64)  [21] q_cap
  *   [22] device out (n_cols doubles + 4 int64)  [23] pinned host out (same)
- *   [24] int32 counter  [25] stream (optional)
+ *   [24] int32 counter  [25] stream (optional)  [26] E_c  [27] n_c  [28] ldEc
+ *   (optional: compacted corpus rows for the TMA cost build, 0 = none)
  * swmd_plan_run: select (host) -> H2D -> cost build -> solve -> D2H -> sync;
  * copies the distances to wmd_host and the error record to err_host and the
  * cost / solve device times (ms) to times_ms[0..1] and the host select time

@@ -46,6 +46,8 @@ _SIGS = {
     "swmd_cost_build_f64": [_P, _I64, _I32, _I64, _P, _I32, _P, _D, _I32, _P, _P, _I64,
                             _P, _P, _P, _P, _I64, _P],
     "swmd_precompute_f64": [_P, _I64, _I32, _I64, _P, _D, _P, _P, _P, _P],
+    "swmd_cost_build_compact_f64": [_P, _I64, _P, _I64, _I32, _I64, _P, _P, _I32, _P, _D, _P,
+                                    _P, _P, _I64, _P],
     "swmd_solve_f64": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
                        _I64, _I64, _I32, _I32, _P, _P, _P],
     "swmd_fused_iteration_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _P],
@@ -86,7 +88,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
 def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
-        _lib = load()
+        _lib = load(os.environ.get("SWMD_LIB", LIB_PATH))   # override: build experiments
     return _lib
 
 

@@ -121,6 +121,25 @@ class DeviceCorpus:
             store[key] = dc
         return dc
 
+    def compact_rows(self, de) -> "tuple[torch.Tensor, int] | None":
+        """The corpus's vocabulary rows of ``de`` as one contiguous f64 matrix
+        (cached per embedding table): the TMA cost build streams it.  Identity
+        (the table itself) when every row occurs."""
+        if de.dtype != torch.float64 or de.dim % 2 or de.ld % 2:
+            return None
+        cache = self.__dict__.setdefault("_compact", {})
+        hit = cache.get(id(de))
+        if hit is not None and hit[0] is de:
+            return hit[1], hit[2]
+        if self.present_rows is None or self.n_present >= self.n_rows:
+            Ec, ld = de.E, de.ld
+        else:
+            Ec = de.E.index_select(0, self.present_rows.long()).contiguous()
+            ld = int(Ec.stride(0))
+        cache.clear()
+        cache[id(de)] = (de, Ec, ld)
+        return Ec, ld
+
     def ensure_pos(self):
         if self._pos_host is None and hasattr(self, "_pos_host_fn"):
             self._pos_host = self._pos_host_fn()[2]

@@ -348,6 +348,17 @@ class QueryPlan:
 
     def enqueue_distances(self) -> None:
         dc, de = self.dc, self.de
+        comp = dc.compact_rows(de) if self.mode == COST_MODE_GRAM else None
+        if comp is not None:
+            Ec, ldc = comp
+            n_c = dc.n_present if self.use_list else dc.n_rows
+            _lib.call("swmd_cost_build_compact_f64", de.E.data_ptr(), de.ld, Ec.data_ptr(), n_c,
+                      de.dim, ldc, dc.present_rows.data_ptr() if self.use_list else None,
+                      self.sel_dev.data_ptr(), self.v_r, self.r_dev.data_ptr(),
+                      float(self.config.lam), self.norms.data_ptr(), self.K.data_ptr(),
+                      self.KM.data_ptr(), self.ldk, self.stream)
+            self.launches += (self.ldk + 31) // 32
+            return
         _lib.call("swmd_cost_build_f64", de.E.data_ptr(), de.V, de.dim, de.ld,
                   self.sel_dev.data_ptr(), self.v_r, self.r_dev.data_ptr(),
                   float(self.config.lam), self.mode,
@@ -534,13 +545,21 @@ class NativePlan:
             self.K.data_ptr(), self.KM.data_ptr(), V * 32,
             self.qdev.data_ptr(), self.qhost.data_ptr(), self.Q_CAP,
             self.out_dev.data_ptr(), self.out_host.data_ptr(), self.counter.data_ptr(),
-            stream_ptr(dev)], dtype=np.int64)
+            stream_ptr(dev), *self._compact(dc, de)], dtype=np.int64)
         import ctypes
         h = ctypes.c_void_p()
         _lib.call("swmd_plan_create", ctypes.byref(h), desc.ctypes.data, desc.size)
         self.handle = h
         self._args = (self.err.ctypes.data, self.times.ctypes.data, self.vr.ctypes.data)
         self._stream = stream_ptr(dev)
+
+    def _compact(self, dc, de):
+        comp = dc.compact_rows(de)
+        if comp is None:
+            return [0, 0, 0]
+        self._Ec = comp[0]
+        n_c = dc.n_present if (dc.present_rows is not None and dc.n_present < dc.n_rows) else dc.n_rows
+        return [comp[0].data_ptr(), n_c, comp[1]]
 
     def __del__(self):
         try:
