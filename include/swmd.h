@@ -235,6 +235,18 @@ int swmd_plan_run(swmd_plan* plan, const double* query, int64_t V, double lam,
                   int32_t max_iter, int32_t cost_mode, double* wmd_host,
                   int64_t* err_host, float* times_ms, int64_t* v_r_out);
 
+/*
+ * Device top-k of a distance vector (north_star: identical top-k document
+ * indices): the k <= 1024 smallest values in ascending order, ties broken
+ * toward the lower index — exactly np.argsort(values, kind="stable")[:k]
+ * (NaN sorts last).  out_idx receives index + index_offset.  scratch must
+ * hold swmd_topk_scratch_bytes(n, k) bytes of device memory.
+ */
+int swmd_topk_f64(const double* values, int64_t n, int32_t k, int64_t index_offset,
+                  int64_t* out_idx, double* out_val, void* scratch, int64_t scratch_bytes,
+                  void* stream);
+int64_t swmd_topk_scratch_bytes(int64_t n, int32_t k);
+
 /* Flush helper for benchmarks: writes `bytes` of scratch (> L2 evicts
  * everything) and reads it back, leaving L2 clean (no dirty write-back is
  * charged to the next kernel). */

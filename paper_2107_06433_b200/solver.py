@@ -55,6 +55,8 @@ __all__ = [
     "DegEvent",
     "ShardResult",
     "QueryPlan",
+    "TopKResult",
+    "sinkhorn_wmd_topk",
 ]
 
 PHASES = ("select", "distances", "precompute", "init", "iterations", "final", "total")
@@ -647,6 +649,77 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
     host = {"select": t_select, "total": time.perf_counter() - t_start}
     return SolverResult(wmd=res.wmd, iterations_run=res.iterations, converged=res.converged,
                         timings=LazyTimings(host, spans, ev))
+
+
+@dataclass(frozen=True)
+class TopKResult:
+    """The k nearest documents of one query: ``indices`` ascending by distance,
+    ties toward the lower document id (np.argsort(wmd, kind="stable")[:k]),
+    and their distances ``wmd``."""
+
+    indices: np.ndarray
+    wmd: np.ndarray
+    iterations_run: int
+    converged: bool
+    timings: Mapping
+
+
+def sinkhorn_wmd_topk(query, corpus, embeddings, config: SolverConfig, k: int,
+                      workspace: SinkhornWorkspace | None = None) -> TopKResult:
+    """``sinkhorn_wmd`` followed by a device top-k: only the k nearest
+    documents cross PCIe (k <= 1024; fp64 path)."""
+    t_start = time.perf_counter()
+    if not 1 <= int(k) <= 1024:
+        raise ValueError(f"k must be in [1, 1024], got {k}")
+    if config.precision != "f64":
+        raise ValueError("sinkhorn_wmd_topk runs the fp64 path")
+    if isinstance(query, SparseVector):
+        query = query.to_dense()
+    query = np.asarray(query, dtype=np.float64)
+    n_vocab = corpus.n_rows
+    if query.shape != (n_vocab,) or tuple(embeddings.shape)[0] != n_vocab:
+        raise ValueError(
+            f"shape mismatch: query {query.shape}, embeddings "
+            f"{tuple(embeddings.shape)}, corpus rows {n_vocab}")
+    ws = workspace if workspace is not None else _default_ws()
+    t0 = time.perf_counter()
+    v_r = _stage_query(query, n_vocab, ws)
+    t_select = time.perf_counter() - t0
+    dev = device()
+    dc = DeviceCorpus.of(corpus, dev)
+    de = DeviceEmbeddings.of(embeddings, dev)
+    ev = _Events(True)
+    plan = QueryPlan(None, None, dc, de, config, ws, staged_v_r=v_r)
+    ev.mark("d0")
+    plan.enqueue_distances()
+    ev.mark("d1")
+    if config.tol is None:
+        plan.enqueue_solve()
+        iterations, converged = config.max_iter, False
+    else:
+        iterations, converged = plan.run_tol()
+    ev.mark("i1")
+    k = min(int(k), dc.n_cols)
+    dws = plan.dws
+    nb = int(_lib.lib().swmd_topk_scratch_bytes(dc.n_cols, k))
+    scratch = dws.flat("topk_scratch", (nb + 7) // 8, torch.int64)
+    res = dws.flat("topk_out", 2 * k, torch.int64)
+    _lib.call("swmd_topk_f64", plan.wmd.data_ptr(), dc.n_cols, k, dc.col_offset,
+              res.data_ptr(), res.data_ptr() + 8 * k, scratch.data_ptr(), nb, plan.stream)
+    host = ws.pinned("topk_host", 2 * k + _lib.ERR_WORDS, torch.int64)
+    host[: 2 * k].copy_(res, non_blocking=True)
+    host[2 * k:].copy_(plan.err, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    hn = host.numpy()
+    event = plan.decode_event(hn[2 * k:].copy())
+    if event is not None:
+        raise DegeneracyError(event.message)
+    spans = {"distances": ("d0", "d1"), "precompute": 0.0, "init": 0.0,
+             "iterations": ("d1", "i1"), "final": 0.0}
+    host_t = {"select": t_select, "total": time.perf_counter() - t_start}
+    return TopKResult(indices=hn[:k].copy(), wmd=hn[k: 2 * k].view(np.float64).copy(),
+                      iterations_run=iterations, converged=converged,
+                      timings=LazyTimings(host_t, spans, ev))
 
 
 def sinkhorn_wmd_batch(queries, corpus, embeddings, config: SolverConfig,

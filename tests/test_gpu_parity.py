@@ -398,3 +398,36 @@ def test_fp32_batch_contract(oracle_lib):
     tol = swmd.sinkhorn_wmd(queries[3], corpus, emb,
                             swmd.SolverConfig(lam=1.0, max_iter=300, tol=1e-6, precision="f32"))
     assert tol.converged and tol.iterations_run < 300
+
+
+# -- device top-k ---------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,k", [("c1", 10), ("c2", 100), ("c2", 1024)])
+def test_topk_matches_stable_argsort(name, k):
+    inst = synth.zipf_instance(name)
+    corpus = inst.corpus()
+    cfg = swmd.SolverConfig()
+    full = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
+    top = swmd.sinkhorn_wmd_topk(inst.query, corpus, inst.embeddings, cfg, k)
+    want = np.argsort(full, kind="stable")[:k]
+    assert np.array_equal(top.indices, want)
+    assert np.array_equal(top.wmd, full[want])
+    g = golden(name)
+    assert _topk_equal(full, g["wmd"], min(k, 100))
+
+
+def test_topk_ties_go_to_lower_index():
+    # identical documents give exactly equal distances (test_ingest.py:119-122)
+    inst = synth.zipf_instance("c1", n_docs=50)
+    cp, rows, vals = inst.col_ptr, inst.rows, inst.vals
+    a, b = cp[7], cp[8]
+    reps = 30
+    cp2 = np.concatenate([cp, cp[-1] + (b - a) * np.arange(1, reps + 1)])
+    rows2 = np.concatenate([rows] + [rows[a:b]] * reps)
+    vals2 = np.concatenate([vals] + [vals[a:b]] * reps)
+    corpus = CsrMatrix.from_csc(inst.n_vocab, 50 + reps, cp2, rows2, vals2)
+    cfg = swmd.SolverConfig()
+    full = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
+    assert np.all(full[50:] == full[7])
+    top = swmd.sinkhorn_wmd_topk(inst.query, corpus, inst.embeddings, cfg, 40)
+    assert np.array_equal(top.indices, np.argsort(full, kind="stable")[:40])
