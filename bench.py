@@ -63,6 +63,9 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        """Launch the sampler and return once it is producing samples; the
+        window opens at return (the caller enters its timed region next)."""
+        self.lines = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -70,17 +73,35 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+        self.reader = threading.Thread(target=self._read, daemon=True)
+        self.reader.start()
+        deadline = time.perf_counter() + 5.0
+        while not self.lines and time.perf_counter() < deadline:
+            time.sleep(0.005)
+        self.t0 = time.perf_counter()
         return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append((time.perf_counter(), ln))
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        t1 = time.perf_counter()
+        deadline = t1 + 1.0          # the first sample after the window closes still counts
+        while time.perf_counter() < deadline and not any(ts >= t1 for ts, _ in self.lines):
+            time.sleep(0.005)
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=10)
+            self.proc.wait(timeout=10)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-            out, _ = self.proc.communicate()
+        self.reader.join(timeout=2)
+        after = [ts for ts, _ in self.lines if ts >= t1]
+        t_last = after[0] if after else t1
+        out = "".join(ln for ts, ln in self.lines if self.t0 <= ts <= t_last)
         samples = [[v.strip() for v in ln.split(",")] for ln in out.splitlines() if ln.strip()]
         samples = [x for x in samples if len(x) >= 7]
         if not samples:
@@ -197,6 +218,31 @@ def _cpu_baseline(inst, cfg) -> dict:
             "kind": "port",
             "sample": f"{reps} full {cfg.name} solves, {t_total:.2f}s (oracle/swmd_oracle.c, "
                       f"{cores} OpenMP threads, deterministic column blocks)"}
+
+
+def _transpose_times(inst, dev) -> dict:
+    """A row-major corpus made resident: CSR upload + device transpose
+    (DeviceCorpus.from_csr) beside the reference's host argsort transpose
+    (CsrMatrix.csc_index, sparse.py:98-120).  Not part of the step."""
+    import torch
+
+    from paper_2107_06433_b200 import synth
+    from paper_2107_06433_b200.device import DeviceCorpus
+    from paper_2107_06433_b200.sparse import CsrMatrix
+
+    rp, ci, v = synth.csc_to_csr(inst.n_vocab, inst.n_docs, inst.col_ptr, inst.rows, inst.vals)
+    for _ in range(2):
+        DeviceCorpus.from_csr(inst.n_vocab, inst.n_docs, rp, ci, v, dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    DeviceCorpus.from_csr(inst.n_vocab, inst.n_docs, rp, ci, v, dev)
+    torch.cuda.synchronize()
+    t_dev = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    CsrMatrix(inst.n_vocab, inst.n_docs, rp, ci, v).csc_index()
+    t_host = time.perf_counter() - t0
+    return {"device_ms": 1e3 * t_dev, "host_argsort_ms": 1e3 * t_host, "nnz": int(inst.nnz),
+            "note": "device = pageable CSR upload + swmd_csr_to_csc_f64 + col_ptr readback"}
 
 
 def run_b200(args):
@@ -375,6 +421,8 @@ def run_b200(args):
         "gpu_launches": int(launches),
         "clocks": clock_info,
     }
+    if world == 1:
+        line["corpus_transpose"] = _transpose_times(inst, dev)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline(inst, cfg)
     print(json.dumps(line), flush=True)

@@ -236,6 +236,22 @@ int swmd_plan_run(swmd_plan* plan, const double* query, int64_t V, double lam,
                   int64_t* err_host, float* times_ms, int64_t* v_r_out);
 
 /*
+ * Device CSR -> CSC transpose (replaces the host argsort of
+ * CsrMatrix.csc_index, sparse.py:98-120): from row_ptr (n_rows+1), col_idx,
+ * vals (nnz) to col_ptr (n_cols+1), rows (int32), cvals and pos (the CSR
+ * position of each CSC slot), rows ascending inside each column — identical
+ * to the host transpose.  Columns longer than 1024 entries are left unsorted
+ * and the longest such length is written to *longest_unsorted (0: all done);
+ * the caller then sorts those on the host.  scratch: device memory of
+ * swmd_csr_to_csc_scratch_bytes(n_cols) bytes.
+ */
+int swmd_csr_to_csc_f64(const int64_t* row_ptr, const int64_t* col_idx, const double* vals,
+                        int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t* col_ptr,
+                        int32_t* rows, double* cvals, int64_t* pos, void* scratch,
+                        int64_t scratch_bytes, int32_t* longest_unsorted, void* stream);
+int64_t swmd_csr_to_csc_scratch_bytes(int64_t n_cols);
+
+/*
  * Device top-k of a distance vector (north_star: identical top-k document
  * indices): the k <= 1024 smallest values in ascending order, ties broken
  * toward the lower index — exactly np.argsort(values, kind="stable")[:k]

@@ -63,12 +63,15 @@ _SIGS = {
     "swmd_solve_f32": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
                        _I64, _I64, _I32, _P, _P, _P],
     "swmd_topk_f64": [_P, _I64, _I32, _I64, _P, _P, _P, _I64, _P],
+    "swmd_csr_to_csc_f64": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _P],
+    "swmd_csr_to_csc_scratch_bytes": [_I64],
     "swmd_topk_scratch_bytes": [_I64, _I32],
     "swmd_plan_create": [_P, _P, _I32],
     "swmd_plan_destroy": [_P],
     "swmd_plan_run": [_P, _P, _I64, _D, _I32, _I32, _P, _P, _P, _P],
 }
-_RESTYPE = {"swmd_select_query": ctypes.c_int64, "swmd_topk_scratch_bytes": ctypes.c_int64}
+_RESTYPE = {"swmd_select_query": ctypes.c_int64, "swmd_topk_scratch_bytes": ctypes.c_int64,
+            "swmd_csr_to_csc_scratch_bytes": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGS)
 

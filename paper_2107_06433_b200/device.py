@@ -20,6 +20,7 @@ its row norms f64 (V).
 
 from __future__ import annotations
 
+import warnings
 import weakref
 import zlib
 
@@ -44,7 +45,9 @@ def stream_ptr(dev: torch.device | None = None) -> int:
 
 
 def _h2d(a: np.ndarray, dev: torch.device, dtype: torch.dtype | None = None) -> torch.Tensor:
-    t = torch.from_numpy(np.ascontiguousarray(a))
+    with warnings.catch_warnings():   # read-only host arrays: only read here
+        warnings.simplefilter("ignore", UserWarning)
+        t = torch.from_numpy(np.ascontiguousarray(a))
     if dtype is not None:
         t = t.to(dtype)
     return t.to(dev, non_blocking=False)
@@ -64,23 +67,73 @@ class DeviceCorpus:
         self.device = dev
         base = int(col_ptr[0])
         cp = np.asarray(col_ptr, dtype=np.int64) - base
+        self.col_ptr = _h2d(cp, dev)
+        self.rows = _h2d(np.asarray(rows[base: base + self.nnz], dtype=np.int32), dev)
+        self.vals = _h2d(np.asarray(vals[base: base + self.nnz], dtype=np.float64), dev)
+        present = np.flatnonzero(np.bincount(np.asarray(rows[base: base + self.nnz]),
+                                             minlength=self.n_rows) > 0).astype(np.int32)
+        self._set_layout(cp, present)
+        self._pos_host = pos
+        self._pos = None
+
+    def _set_layout(self, cp: np.ndarray, present: np.ndarray):
         lens = np.diff(cp)
         self.host_col_ptr = cp
         self.mean_len = float(self.nnz / max(1, self.n_cols))
         self.max_len = int(lens.max()) if lens.size else 0
-        self.col_ptr = _h2d(cp, dev)
-        self.rows = _h2d(np.asarray(rows[base: base + self.nnz], dtype=np.int32), dev)
-        self.vals = _h2d(np.asarray(vals[base: base + self.nnz], dtype=np.float64), dev)
         # longest columns first: keeps a warp's columns the same length and
         # leaves the short ones for the tail of the persistent launch
         order = np.argsort(-lens, kind="stable").astype(np.int32)
-        self.order = _h2d(order, dev)
-        present = np.flatnonzero(np.bincount(np.asarray(rows[base: base + self.nnz]),
-                                             minlength=self.n_rows) > 0).astype(np.int32)
+        self.order = _h2d(order, self.device)
         self.n_present = int(present.size)
-        self.present_rows = _h2d(present, dev) if present.size else None
-        self._pos_host = pos
-        self._pos = None
+        self.present_rows = _h2d(present, self.device) if present.size else None
+
+    @classmethod
+    def from_csr(cls, n_rows: int, n_cols: int, row_ptr: np.ndarray, col_idx: np.ndarray,
+                 values: np.ndarray, dev: torch.device) -> "DeviceCorpus":
+        """Upload the CSR arrays and transpose them in HBM (swmd_csr_to_csc_f64).
+
+        Replaces the host argsort of ``CsrMatrix.csc_index`` (sparse.py:98-120)
+        for a corpus that arrives row-major: the CSC (rows ascending within a
+        column, so identical to the host view) and the CSR position of every
+        slot are built by the device; only ``col_ptr`` comes back to size the
+        launch order.
+        """
+        rp = np.asarray(row_ptr, dtype=np.int64)
+        nnz = int(rp[-1]) if rp.size else 0
+        self = cls.__new__(cls)
+        self.n_rows, self.n_cols, self.nnz = int(n_rows), int(n_cols), nnz
+        self.col_offset, self.n_key, self.device = 0, int(n_cols), dev
+        d_rp = _h2d(rp, dev)
+        d_ci = _h2d(np.asarray(col_idx, dtype=np.int64), dev)
+        d_v = _h2d(np.asarray(values, dtype=np.float64), dev)
+        self.col_ptr = torch.empty(self.n_cols + 1, dtype=torch.int64, device=dev)
+        self.rows = torch.empty(max(1, nnz), dtype=torch.int32, device=dev)[:nnz]
+        self.vals = torch.empty(max(1, nnz), dtype=torch.float64, device=dev)[:nnz]
+        pos = torch.empty(max(1, nnz), dtype=torch.int64, device=dev)[:nnz]
+        sb = int(_lib.lib().swmd_csr_to_csc_scratch_bytes(self.n_cols))
+        scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+        longest = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("swmd_csr_to_csc_f64", d_rp.data_ptr(), d_ci.data_ptr(), d_v.data_ptr(),
+                  self.n_rows, self.n_cols, nnz, self.col_ptr.data_ptr(), self.rows.data_ptr(),
+                  self.vals.data_ptr(), pos.data_ptr(), scratch.data_ptr(), sb,
+                  longest.data_ptr(), stream_ptr(dev))
+        cp = self.col_ptr.cpu().numpy()
+        if int(longest.item()) > 0:
+            # the few columns longer than the warp sort handles: sort their
+            # slots by CSR position on the device
+            long_cols = np.flatnonzero(np.diff(cp) > 1024)
+            for c in long_cols:
+                b, e = int(cp[c]), int(cp[c + 1])
+                perm = torch.argsort(pos[b:e], stable=True)
+                pos[b:e] = pos[b:e][perm]
+                self.rows[b:e] = self.rows[b:e][perm]
+                self.vals[b:e] = self.vals[b:e][perm]
+        present = np.flatnonzero(np.diff(rp) > 0).astype(np.int32)
+        self._set_layout(cp, present)
+        self._pos_host = None
+        self._pos = pos
+        return self
 
     @property
     def pos(self) -> torch.Tensor:
@@ -109,6 +162,10 @@ class DeviceCorpus:
                 except TypeError:
                     pass
         dc = store.get(key)
+        if dc is None and _row_major_only(corpus):
+            dc = cls.from_csr(corpus.n_rows, corpus.n_cols, corpus.row_ptr, corpus.col_idx,
+                              corpus.values, dev)
+            store[key] = dc
         if dc is None:
             if hasattr(corpus, "csc_compact"):
                 cp, rows, vals = corpus.csc_compact()
@@ -144,6 +201,16 @@ class DeviceCorpus:
         if self._pos_host is None and hasattr(self, "_pos_host_fn"):
             self._pos_host = self._pos_host_fn()[2]
         return self.pos
+
+def _row_major_only(corpus) -> bool:
+    """True for a corpus that holds only its CSR arrays (no column view has
+    been built on the host yet): it is transposed on the device."""
+    if getattr(corpus, "_csc_cache", None) is not None:
+        return False
+    if hasattr(corpus, "csc_compact"):
+        return corpus._csc_compact is None and corpus._csr is not None
+    return hasattr(corpus, "row_ptr") and hasattr(corpus, "col_idx")
+
 
 def _fingerprint(a: np.ndarray) -> int:
     """Cheap content check of a cached table: 256 strided elements plus the

@@ -431,3 +431,72 @@ def test_topk_ties_go_to_lower_index():
     assert np.all(full[50:] == full[7])
     top = swmd.sinkhorn_wmd_topk(inst.query, corpus, inst.embeddings, cfg, 40)
     assert np.array_equal(top.indices, np.argsort(full, kind="stable")[:40])
+
+
+# -- device CSR -> CSC transpose (replaces the host argsort of sparse.py:98-120) --------------
+
+def _device_csc(corpus):
+    import torch
+    from paper_2107_06433_b200.device import DeviceCorpus
+
+    dc = DeviceCorpus.from_csr(corpus.n_rows, corpus.n_cols, corpus.row_ptr, corpus.col_idx,
+                               corpus.values, torch.device("cuda", 0))
+    return (dc.col_ptr.cpu().numpy(), dc.rows.cpu().numpy(), dc.pos.cpu().numpy(),
+            dc.vals.cpu().numpy(), dc)
+
+
+def _host_csc(corpus):
+    rp, ci, v = corpus.row_ptr, corpus.col_idx, corpus.values
+    return CsrMatrix(corpus.n_rows, corpus.n_cols, rp, ci, v).csc_index()
+
+
+def _assert_same_csc(corpus):
+    cp, rows, pos, vals, dc = _device_csc(corpus)
+    hcp, hrows, hpos, hvals = _host_csc(corpus)
+    assert np.array_equal(cp, hcp)
+    assert np.array_equal(rows, hrows.astype(np.int32))
+    assert np.array_equal(pos, hpos)
+    assert np.array_equal(vals, hvals)
+    present = np.flatnonzero(np.diff(corpus.row_ptr) > 0)
+    assert dc.n_present == present.size
+    return dc
+
+
+def test_device_csc_matches_host_small(small_golden):
+    for k in range(50):
+        _, corpus, _ = small_instance(small_golden, k)
+        _assert_same_csc(corpus)
+
+
+def test_device_csc_matches_host_c2():
+    inst = synth.zipf_instance("c2")
+    rp, ci, v = synth.csc_to_csr(inst.n_vocab, inst.n_docs, inst.col_ptr, inst.rows, inst.vals)
+    corpus = CsrMatrix(inst.n_vocab, inst.n_docs, rp, ci, v)
+    _assert_same_csc(corpus)
+
+
+def test_device_csc_long_and_empty_columns():
+    rng = np.random.default_rng(11)
+    V, N = 6000, 40
+    trip = []
+    lens = [0, 1, 33, 257, 1024, 1025, 3000, 0, 5] + list(rng.integers(0, 70, N - 9))
+    for j, L in enumerate(lens):
+        for i in np.sort(rng.choice(V, size=int(L), replace=False)):
+            trip.append((int(i), j, float(rng.integers(1, 5))))
+    corpus = csr_from_triplets(trip, V, N)
+    _assert_same_csc(corpus)
+    empty = csr_from_triplets([], 7, 3)
+    cp, rows, pos, vals, dc = _device_csc(empty)
+    assert np.array_equal(cp, np.zeros(4, dtype=np.int64)) and rows.size == 0
+    assert dc.n_present == 0
+
+
+def test_csr_corpus_solves_through_device_transpose():
+    g = golden("c2")
+    inst = synth.zipf_instance("c2")
+    rp, ci, v = synth.csc_to_csr(inst.n_vocab, inst.n_docs, inst.col_ptr, inst.rows, inst.vals)
+    corpus = CsrMatrix(inst.n_vocab, inst.n_docs, rp, ci, v)
+    res = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings,
+                            swmd.SolverConfig(lam=10.0, max_iter=15))
+    assert corpus._csc_cache is None          # no host transpose happened
+    assert max_rel_err(res.wmd, g["wmd"]) <= RTOL
