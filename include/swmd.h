@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SWMD_ABI_VERSION 1
+#define SWMD_ABI_VERSION 2
 
 #define SWMD_EINVAL 1000      /* bad size / null pointer / misaligned buffer */
 #define SWMD_EVR 1001         /* v_r outside what this entry point supports */
@@ -218,13 +218,16 @@ int64_t swmd_select_query(const double* r, int64_t n, int64_t* stage, int64_t ca
  *   [12] col_key_offset  [13] n_key  [14] max_len  [15] group_hint
  *   [16] K  [17] KM  [18] K/KM capacity (doubles)  [19] device stage (2*q_cap
  *   int64)  [20] pinned host stage (2*q_cap int64)  [21] q_cap
- *   [22] device out (n_cols doubles + 4 int64)  [23] pinned host out (same)
+ *   [22] device out (n_cols doubles + 4 int64 error record + 3 int64 device
+ *   clock stamps)  [23] pinned host out (same)
  *   [24] int32 counter  [25] stream (optional)  [26] E_c  [27] n_c  [28] ldEc
  *   (optional: compacted corpus rows for the TMA cost build, 0 = none)
  * swmd_plan_run: select (host) -> H2D -> cost build -> solve -> D2H -> sync;
  * copies the distances to wmd_host and the error record to err_host and the
- * cost / solve device times (ms) to times_ms[0..1] and the host select time
- * (ms) to times_ms[2].  Returns 0, a CUDA
+ * cost / solve device times (ms) to times_ms[0..1]; host times (ms, from
+ * entry) to times_ms[2] (select done), [3] (all work enqueued), [4] (stream
+ * synchronised), [5] (results copied out) — times_ms holds 6 floats or is
+ * NULL.  Returns 0, a CUDA
  * error, -2 (negative query entry), -3 (no positive entry) or -4 (query
  * outside the plan's fast path: the caller uses the general entry points).
  */

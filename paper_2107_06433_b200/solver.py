@@ -531,11 +531,11 @@ class NativePlan:
         self.KM = torch.empty(V * 32, dtype=torch.float64, device=dev)
         self.qdev = torch.empty(2 * self.Q_CAP, dtype=torch.int64, device=dev)
         self.qhost = torch.empty(2 * self.Q_CAP, dtype=torch.int64, pin_memory=True)
-        self.out_dev = torch.empty(N + _lib.ERR_WORDS, dtype=torch.int64, device=dev)
-        self.out_host = torch.empty(N + _lib.ERR_WORDS, dtype=torch.int64, pin_memory=True)
+        self.out_dev = torch.empty(N + _lib.ERR_WORDS + 3, dtype=torch.int64, device=dev)
+        self.out_host = torch.empty(N + _lib.ERR_WORDS + 3, dtype=torch.int64, pin_memory=True)
         self.counter = torch.empty(1, dtype=torch.int32, device=dev)
         self.err = np.empty(_lib.ERR_WORDS, dtype=np.int64)
-        self.times = np.zeros(3, dtype=np.float32)
+        self.times = np.zeros(6, dtype=np.float32)
         self.vr = np.zeros(1, dtype=np.int64)
         norms = de.norms
         pres = dc.present_rows

@@ -8,6 +8,7 @@ for spec in "$@"; do
   export SWMD_SOLVE_KERNEL=${pick:-}
   [ -z "$SWMD_LIB" ] && unset SWMD_LIB
   [ -z "$SWMD_SOLVE_KERNEL" ] && unset SWMD_SOLVE_KERNEL
+  timeout 300 python scripts/parity_report.py c1 c2 c3 > gpurun_out/var_${label}_parity.log 2>&1; cat gpurun_out/var_${label}_parity.log | sed "s/^/$label /"
   timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "solver or c2 or c3 or config or zero or tol or shard or column" > gpurun_out/var_${label}_test.log 2>&1
   echo "$label tests rc=$? $(tail -1 gpurun_out/var_${label}_test.log)"
   for cfg in c2 c3; do

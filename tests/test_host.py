@@ -40,7 +40,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.EXPORTED)
-    assert lib.swmd_abi_version() == 1
+    assert lib.swmd_abi_version() == 2
 
 
 def test_library_is_sm100a():
