@@ -377,7 +377,7 @@ def run_b200(args):
             ncu = json.load(f)["kernels"]
     except (OSError, KeyError, ValueError):
         pass
-    kname = "hybrid_solve" if dominant == "solve" else "cost_tmap_kernel"
+    kname = "reg_solve" if dominant == "solve" else "cost_tmap_kernel"
     traffic = None
     if kname in ncu and args.config == "c2" and world == 1:
         traffic = ncu[kname]["dram_read_bytes"] + ncu[kname]["dram_write_bytes"]
@@ -385,6 +385,28 @@ def run_b200(args):
         achieved = solve_bytes / (s_ms / 1e3) / 1e9
     else:
         achieved = cost_bytes / (c_ms / 1e3) / 1e9
+    # the solve against every roofline the survey names (§8d): HBM (canonical,
+    # effective), the K-row gather against the measured L2 gather peak, FP64
+    probes = {}
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_probes.json")) as f:
+            probes = json.load(f)
+    except (OSError, ValueError):
+        pass
+    l2_peak = float(probes.get("l2_gather_2kb_rows_tbs", 18.9)) * 1e3
+    fp64_peak = float(probes.get("fp64_dmma_tflops", 36.9)) * 1e3
+    t_hbm = solve_bytes / hbm / 1e3               # us at peak
+    t_l2 = gather_l2 / l2_peak / 1e3
+    t_fp64 = flops / fp64_peak / 1e3
+    bind = max((t_hbm, "hbm"), (t_l2, "l2_gather"), (t_fp64, "fp64"))
+    binding = {
+        "resource": bind[1], "t_hbm_us": t_hbm, "t_l2_us": t_l2, "t_fp64_us": t_fp64,
+        "solve_us": 1e3 * s_ms, "frac": bind[0] / (1e3 * s_ms),
+        "peaks": {"hbm_gbs": hbm, "l2_gather_gbs": l2_peak, "fp64_gflops": fp64_peak},
+        "note": "binding roofline = max(T_HBM, T_L2, T_FP64) for the persistent solve (SURVEY §8d); "
+                "L2 and FP64 peaks measured by scripts/l2_probe.cu and scripts/dmma_probe.cu "
+                "(profiles/r01_probes.json)",
+    }
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -406,6 +428,7 @@ def run_b200(args):
                      "an effective figure)") if dominant == "solve" else
                     "cost bytes = E rows of words present in the corpus + K, K*M writes",
         },
+        "solve_binding_roofline": binding,
         "kernels": {
             "cost_build_ms": c_ms, "cost_build_gbs": cost_bytes / (c_ms / 1e3) / 1e9,
             "solve_ms": s_ms, "solve_eff_hbm_gbs": solve_bytes / (s_ms / 1e3) / 1e9,
