@@ -271,6 +271,11 @@ int64_t swmd_topk_scratch_bytes(int64_t n, int32_t k);
  * charged to the next kernel). */
 int swmd_l2_flush(void* scratch, int64_t bytes, void* stream);
 
+/* Host helper: a multiply-xorshift hash of 64 strided elements + the last 16 of a host
+ * array (n elements of itemsize bytes) — the in-place-edit check of the
+ * resident embedding-table cache (device.py). */
+int64_t swmd_sample_crc(const void* data, int64_t n, int64_t itemsize);
+
 #ifdef __cplusplus
 }
 #endif

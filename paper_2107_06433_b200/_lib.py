@@ -65,13 +65,15 @@ _SIGS = {
     "swmd_topk_f64": [_P, _I64, _I32, _I64, _P, _P, _P, _I64, _P],
     "swmd_csr_to_csc_f64": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _P],
     "swmd_csr_to_csc_scratch_bytes": [_I64],
+    "swmd_sample_crc": [_P, _I64, _I64],
     "swmd_topk_scratch_bytes": [_I64, _I32],
     "swmd_plan_create": [_P, _P, _I32],
     "swmd_plan_destroy": [_P],
     "swmd_plan_run": [_P, _P, _I64, _D, _I32, _I32, _P, _P, _P, _P],
 }
 _RESTYPE = {"swmd_select_query": ctypes.c_int64, "swmd_topk_scratch_bytes": ctypes.c_int64,
-            "swmd_csr_to_csc_scratch_bytes": ctypes.c_int64}
+            "swmd_csr_to_csc_scratch_bytes": ctypes.c_int64,
+            "swmd_sample_crc": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGS)
 
@@ -95,6 +97,13 @@ def lib() -> ctypes.CDLL:
     if _lib is None:
         _lib = load(os.environ.get("SWMD_LIB", LIB_PATH))   # override: build experiments
     return _lib
+
+
+def lib_or_none():
+    try:
+        return lib()
+    except (NativeUnavailable, OSError):
+        return None
 
 
 def call(name: str, *args) -> None:

@@ -32,12 +32,28 @@ from . import _lib
 __all__ = ["DeviceCorpus", "DeviceEmbeddings", "device", "stream_ptr", "DeviceWorkspace"]
 
 
+_CUDA_OK = False
+_DEVICES: dict = {}
+
+
+def cuda_ok() -> bool:
+    """torch.cuda.is_available(), remembered once true (per-call cost matters
+    on the per-query path)."""
+    global _CUDA_OK
+    if not _CUDA_OK:
+        _CUDA_OK = torch.cuda.is_available()
+    return _CUDA_OK
+
+
 def device(index: int | None = None) -> torch.device:
-    if not torch.cuda.is_available():
+    if not cuda_ok():
         raise _lib.NativeUnavailable("no CUDA device is visible; the B200 path has no CPU fallback")
     if index is None:
         index = torch.cuda.current_device()
-    return torch.device("cuda", index)
+    d = _DEVICES.get(index)
+    if d is None:
+        d = _DEVICES[index] = torch.device("cuda", index)
+    return d
 
 
 def stream_ptr(dev: torch.device | None = None) -> int:
@@ -222,6 +238,14 @@ def _row_major_only(corpus) -> bool:
 
 
 def _fingerprint(a: np.ndarray) -> int:
+    if a.flags.c_contiguous and a.size >= 16:
+        lib = _lib.lib_or_none()
+        if lib is not None:   # the same sampled CRC, one native call
+            return int(lib.swmd_sample_crc(a.ctypes.data, a.size, a.itemsize))
+    return _fingerprint_py(a)
+
+
+def _fingerprint_py(a: np.ndarray) -> int:
     """Cheap content check of a cached table: 256 strided elements plus the
     last 16, CRC32 — catches an in-place edit of the table without reading it."""
     flat = a.reshape(-1)
@@ -237,6 +261,7 @@ class DeviceEmbeddings:
     """
 
     _cache: dict = {}
+    _last = None
 
     def __init__(self, E: torch.Tensor, dim: int | None = None):
         self.E = E
@@ -281,6 +306,10 @@ class DeviceEmbeddings:
         arr = np.asarray(E)
         if arr.ndim != 2:
             raise ValueError(f"embeddings must be 2-D, got shape {arr.shape}")
+        last = cls._last
+        if (last is not None and last[0] is arr and last[1] == arr.shape and last[2] is dev
+                and last[3] == dtype and last[4] == _fingerprint(arr)):
+            return last[5]            # the same live array object, content unchanged
         key = ("numpy", dev.index, arr.__array_interface__["data"][0], arr.shape,
                arr.strides, arr.dtype.str, _fingerprint(arr), dtype)
         de = cls._cache.get(key)
@@ -298,6 +327,8 @@ class DeviceEmbeddings:
             cls._cache = {k: v for k, v in cls._cache.items()
                           if k[0] == "torch" or k[-1] != dtype}
             cls._cache[key] = de
+        # holding the array keeps its id from being reused while it is cached
+        cls._last = (arr, arr.shape, dev, dtype, key[6], de)
         return de
 
 

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import DeviceCorpus, DeviceEmbeddings, DeviceWorkspace, device, stream_ptr
+from .device import cuda_ok, DeviceCorpus, DeviceEmbeddings, DeviceWorkspace, device, stream_ptr
 from .kernels import (
     COST_MODE_DIRECT,
     COST_MODE_GRAM,
@@ -614,7 +614,7 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
         return res
     if (config.tol is None and isinstance(query, np.ndarray) and query.dtype == np.float64
             and query.ndim == 1 and query.flags.c_contiguous and corpus.n_cols > 0
-            and torch.cuda.is_available()):
+            and cuda_ok()):
         # native runtime: one C call does select -> H2D -> kernels -> D2H
         dev = device()
         dc = DeviceCorpus.of(corpus, dev)
