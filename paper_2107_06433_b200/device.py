@@ -197,27 +197,18 @@ class DeviceCorpus:
     def compact_rows(self, de) -> "tuple[torch.Tensor, int] | None":
         """The corpus's vocabulary rows of ``de`` as one contiguous f64 matrix
         (cached per embedding table): the TMA cost build streams it.  The
-        table itself when every row occurs and its stride already fits."""
+        table itself when every row occurs."""
         if de.dtype != torch.float64 or de.dim % 2 or de.ld % 2:
             return None
         cache = self.__dict__.setdefault("_compact", {})
         hit = cache.get(id(de))
         if hit is not None and hit[0] is de:
             return hit[1], hit[2]
-        # row stride 16 * nchp doubles with nchp odd (zero pad columns): the
-        # cost build then streams 8 whole rows per TMA box (swmd.h)
-        nchp = (de.dim + 15) // 16
-        nchp += 1 - nchp % 2
-        ld = 16 * nchp
         if self.present_rows is None or self.n_present >= self.n_rows:
-            if de.ld == ld:
-                Ec = de.E
-            else:
-                Ec = torch.zeros((de.V, ld), dtype=torch.float64, device=de.E.device)
-                Ec[:, : de.dim].copy_(de.E[:, : de.dim])
+            Ec, ld = de.E, de.ld             # every row occurs: the table itself
         else:
-            Ec = torch.zeros((self.n_present, ld), dtype=torch.float64, device=de.E.device)
-            Ec[:, : de.dim].copy_(de.E.index_select(0, self.present_rows.long())[:, : de.dim])
+            Ec = de.E.index_select(0, self.present_rows.long())[:, : de.dim].contiguous()
+            ld = int(Ec.stride(0))
         cache.clear()
         cache[id(de)] = (de, Ec, ld)
         return Ec, ld
