@@ -500,3 +500,25 @@ def test_csr_corpus_solves_through_device_transpose():
                             swmd.SolverConfig(lam=10.0, max_iter=15))
     assert corpus._csc_cache is None          # no host transpose happened
     assert max_rel_err(res.wmd, g["wmd"]) <= RTOL
+
+
+def test_native_plan_graphs_per_query_shape(oracle_lib):
+    """The native plan caches one CUDA graph per (v_r, lam, max_iter, mode):
+    interleaving query lengths and lambdas must reuse the right one."""
+    rng = np.random.default_rng(77)
+    V, N = 4000, 300
+    emb = synth.normal_embeddings(rng, V, 48)
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, 5, 60)
+    corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+    ws = swmd.SinkhornWorkspace()
+    queries = [synth.zipf_query(rng, V, v) for v in (5, 19, 32, 19, 5)]
+    for rep in range(2):
+        for k, q in enumerate(queries):
+            lam = (10.0, 3.0)[(k + rep) % 2]
+            it = (15, 7)[rep]
+            got = swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig(lam=lam, max_iter=it),
+                                    workspace=ws)
+            want = oracle_lib.solve(q, cp, rows, vals, emb, lam=lam, max_iter=it).wmd
+            assert max_rel_err(got.wmd, want) <= RTOL, (rep, k)
+            assert set(got.timings) >= {"select", "distances", "iterations", "total"}
+            assert got.timings["distances"] > 0 and got.timings["iterations"] > 0
