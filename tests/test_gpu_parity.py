@@ -254,6 +254,29 @@ def test_zero_denominator_in_solver_matches_oracle(oracle_lib):
     assert str(exc.value) == str(want.value)
 
 
+def test_first_zero_denominator_reported_when_one_lane_sees_several(oracle_lib):
+    # two underflowing rows of one column sit in the same lane slot of
+    # consecutive rounds (positions 1 and 17, and 1 and 33 with an 8-lane
+    # round); the reference's CSR walk reports the smaller row
+    V, N = 64, 3
+    emb = np.zeros((V, 2))
+    emb[:, 0] = np.linspace(0.0, 1.0, V)
+    far = [1, 17, 33]
+    emb[far, 1] = 1e3                       # exp(-lam * M) underflows to 0
+    trip = [(i, 0, 1.0 + (i % 3)) for i in range(48)]
+    trip += [(i, 1, 1.0) for i in (0, 2, 5)] + [(i, 2, 2.0) for i in (3, 4)]
+    corpus = csr_from_triplets(trip, V, N)
+    cp, rows, _, vals = corpus.csc_index()
+    q = np.zeros(V)
+    q[[0, 2]] = [0.5, 0.5]
+    with pytest.raises(swmd.DegeneracyError) as exc:
+        swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig(lam=50.0, max_iter=3))
+    with pytest.raises(oracle_lib.OracleDegeneracy) as want:
+        oracle_lib.solve(q, cp, rows, vals, emb, lam=50.0, max_iter=3)
+    assert str(exc.value) == str(want.value)
+    assert "(1, 0)" in str(exc.value)
+
+
 def test_tol_exit_is_self_consistent():
     inst = synth.zipf_instance("c1", n_docs=40)
     corpus = inst.corpus()
