@@ -55,6 +55,9 @@ extern "C" {
 int swmd_abi_version(void);
 int swmd_device_sm_count(void);
 int swmd_err_reset(int64_t* err, void* stream);
+/* error record + solve work counter in one launch; enqueue it before the cost
+ * build so the following swmd_solve_f64_reset_done starts right after it */
+int swmd_solve_reset(int64_t* err, int32_t* counter, void* stream);
 
 /* Row sums of squares of E (V x dim, row stride ldE) — cached per embedding
  * table for the Gram-form cost build. */
@@ -132,6 +135,16 @@ int swmd_solve_f64(const int64_t* col_ptr, const int32_t* rows, const double* va
                    const double* x_in, double* x_out, double* wmd,
                    int64_t col_key_offset, int64_t n_key, int32_t group_hint,
                    int32_t max_len_hint, int64_t* err, int32_t* counter, void* stream);
+/* swmd_solve_f64 whose counter (and error record) were reset by swmd_solve_reset
+ * earlier on the stream: no memset node between the cost build and the solve */
+int swmd_solve_f64_reset_done(const int64_t* col_ptr, const int32_t* rows, const double* vals,
+                              int64_t n_cols, const int32_t* order,
+                              const double* kernel, const double* kernel_cost,
+                              const double* weights, int32_t v_r, int64_t ldk,
+                              int32_t t_begin, int32_t t_end,
+                              const double* x_in, double* x_out, double* wmd,
+                              int64_t col_key_offset, int64_t n_key, int32_t group_hint,
+                              int32_t max_len_hint, int64_t* err, int32_t* counter, void* stream);
 
 /*
  * fp32 multi-query variant (BASELINE config c4; the reference is fp64-only,

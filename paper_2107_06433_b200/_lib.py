@@ -42,6 +42,7 @@ _SIGS = {
     "swmd_abi_version": [],
     "swmd_device_sm_count": [],
     "swmd_err_reset": [_P, _P],
+    "swmd_solve_reset": [_P, _P, _P],
     "swmd_row_norms_f64": [_P, _I64, _I32, _I64, _P, _P],
     "swmd_cost_build_f64": [_P, _I64, _I32, _I64, _P, _I32, _P, _D, _I32, _P, _P, _I64,
                             _P, _P, _P, _P, _I64, _P],
@@ -50,6 +51,8 @@ _SIGS = {
                                     _P, _P, _I64, _P],
     "swmd_solve_f64": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
                        _I64, _I64, _I32, _I32, _P, _P, _P],
+    "swmd_solve_f64_reset_done": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P,
+                                  _P, _P, _I64, _I64, _I32, _I32, _P, _P, _P],
     "swmd_fused_iteration_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _P],
     "swmd_fused_final_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _P],
     "swmd_sddmm_f64": [_P, _P, _P, _P, _I64, _P, _I32, _I64, _P, _P, _I64, _P, _P],

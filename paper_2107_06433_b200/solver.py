@@ -350,6 +350,11 @@ class QueryPlan:
 
     def enqueue_distances(self) -> None:
         dc, de = self.dc, self.de
+        # the solve's error record and work counter are reset here, ahead of
+        # the cost build, so enqueue_solve launches right behind it
+        _lib.call("swmd_solve_reset", self.err.data_ptr(), self.counter.data_ptr(), self.stream)
+        self.launches += 1
+        self._armed = True
         comp = dc.compact_rows(de) if self.mode == COST_MODE_GRAM else None
         if comp is not None:
             Ec, ldc = comp
@@ -370,9 +375,10 @@ class QueryPlan:
                   self.KM.data_ptr(), self.ldk, self.stream)
         self.launches += (self.ldk + 31) // 32
 
-    def _solve(self, t0: int, t1: int, x_in, x_out, wmd) -> None:
+    def _solve(self, t0: int, t1: int, x_in, x_out, wmd, reset_done: bool = False) -> None:
         dc = self.dc
-        _lib.call("swmd_solve_f64", dc.col_ptr.data_ptr(), dc.rows.data_ptr(),
+        _lib.call("swmd_solve_f64_reset_done" if reset_done else "swmd_solve_f64",
+                  dc.col_ptr.data_ptr(), dc.rows.data_ptr(),
                   dc.vals.data_ptr(), dc.n_cols, dc.order.data_ptr(), self.K.data_ptr(),
                   self.KM.data_ptr(), self.r_dev.data_ptr(), self.v_r, self.ldk, t0, t1,
                   x_in.data_ptr() if x_in is not None else None,
@@ -384,6 +390,10 @@ class QueryPlan:
 
     def enqueue_solve(self) -> None:
         """tol unset: the whole loop plus the final pass in one persistent launch."""
+        if getattr(self, "_armed", False):
+            self._armed = False
+            self._solve(0, self.config.max_iter, None, None, self.wmd, reset_done=True)
+            return
         _lib.call("swmd_err_reset", self.err.data_ptr(), self.stream)
         self.launches += 1
         self._solve(0, self.config.max_iter, None, None, self.wmd)
@@ -395,6 +405,7 @@ class QueryPlan:
         n = self.dc.n_cols * self.v_r
         bufs = (self.dws.flat("x_a", n), self.dws.flat("x_b", n))
         host_err = self.ws.pinned("err_host", _lib.ERR_WORDS, torch.int64)
+        self._armed = False
         _lib.call("swmd_err_reset", self.err.data_ptr(), self.stream)
         cur, iterations, converged, failed = None, 0, False, False
         for t in range(cfg.max_iter):
