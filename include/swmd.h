@@ -100,6 +100,14 @@ int swmd_cost_build_compact_f64(const double* E, int64_t ldE, const double* E_c,
                                 const int64_t* sel, int32_t v_r, const double* weights,
                                 double lam, const double* norms, double* kernel,
                                 double* kernel_cost, int64_t ldk, void* stream);
+/* the same build, whose first thread also resets the solve's error record and
+ * work counter (swmd_solve_reset folded into the cost launch) */
+int swmd_cost_build_compact_reset_f64(const double* E, int64_t ldE, const double* E_c,
+                                      int64_t n_c, int32_t dim, int64_t ldEc,
+                                      const int32_t* row_ids, const int64_t* sel, int32_t v_r,
+                                      const double* weights, double lam, const double* norms,
+                                      double* kernel, double* kernel_cost, int64_t ldk,
+                                      int64_t* err, int32_t* counter, void* stream);
 
 /* Elementwise precompute from a given cost matrix: replaces
  * _jit.precompute_mats (_jit.py:105-114) behind kernels.precompute

@@ -49,6 +49,8 @@ _SIGS = {
     "swmd_precompute_f64": [_P, _I64, _I32, _I64, _P, _D, _P, _P, _P, _P],
     "swmd_cost_build_compact_f64": [_P, _I64, _P, _I64, _I32, _I64, _P, _P, _I32, _P, _D, _P,
                                     _P, _P, _I64, _P],
+    "swmd_cost_build_compact_reset_f64": [_P, _I64, _P, _I64, _I32, _I64, _P, _P, _I32, _P, _D,
+                                          _P, _P, _P, _I64, _P, _P, _P],
     "swmd_solve_f64": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
                        _I64, _I64, _I32, _I32, _P, _P, _P],
     "swmd_solve_f64_reset_done": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P,

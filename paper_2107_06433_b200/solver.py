@@ -351,21 +351,23 @@ class QueryPlan:
     def enqueue_distances(self) -> None:
         dc, de = self.dc, self.de
         # the solve's error record and work counter are reset here, ahead of
-        # the cost build, so enqueue_solve launches right behind it
-        _lib.call("swmd_solve_reset", self.err.data_ptr(), self.counter.data_ptr(), self.stream)
-        self.launches += 1
+        # the cost build (by the cost kernel itself on the compact path), so
+        # enqueue_solve launches right behind it
         self._armed = True
         comp = dc.compact_rows(de) if self.mode == COST_MODE_GRAM else None
         if comp is not None:
             Ec, ldc = comp
             n_c = dc.n_present if self.use_list else dc.n_rows
-            _lib.call("swmd_cost_build_compact_f64", de.E.data_ptr(), de.ld, Ec.data_ptr(), n_c,
-                      de.dim, ldc, dc.present_rows.data_ptr() if self.use_list else None,
+            _lib.call("swmd_cost_build_compact_reset_f64", de.E.data_ptr(), de.ld, Ec.data_ptr(),
+                      n_c, de.dim, ldc, dc.present_rows.data_ptr() if self.use_list else None,
                       self.sel_dev.data_ptr(), self.v_r, self.r_dev.data_ptr(),
                       float(self.config.lam), self.norms.data_ptr(), self.K.data_ptr(),
-                      self.KM.data_ptr(), self.ldk, self.stream)
+                      self.KM.data_ptr(), self.ldk, self.err.data_ptr(), self.counter.data_ptr(),
+                      self.stream)
             self.launches += (self.ldk + 31) // 32
             return
+        _lib.call("swmd_solve_reset", self.err.data_ptr(), self.counter.data_ptr(), self.stream)
+        self.launches += 1
         _lib.call("swmd_cost_build_f64", de.E.data_ptr(), de.V, de.dim, de.ld,
                   self.sel_dev.data_ptr(), self.v_r, self.r_dev.data_ptr(),
                   float(self.config.lam), self.mode,
