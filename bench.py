@@ -288,12 +288,13 @@ def run_b200(args):
         if ev is not None:
             ev[2].record()
         if world > 1:
-            gather_in[: c1 - c0].copy_(plan.wmd)
             dist.all_gather_into_tensor(gather_out, gather_in)
         if ev is not None:
             ev[3].record()
 
     plan = QueryPlan(sel, weights, dc, de, scfg, ws)
+    if world > 1:
+        plan.wmd = gather_in[: c1 - c0]    # the solve writes straight into the gather buffer
     for _ in range(max(args.warmup, 3)):
         device_step(plan)
     torch.cuda.synchronize()
@@ -425,7 +426,9 @@ def run_b200(args):
             "bytes_per_launch": solve_bytes if dominant == "solve" else cost_bytes,
             "note": ("solve bytes = survey §8d B_HBM per iteration x iterations + final "
                      "(x round trip counted although the persistent kernel keeps x on chip: "
-                     "an effective figure)") if dominant == "solve" else
+                     "an effective figure); the solve's working set is L2/on-chip resident, "
+                     "so its binding roofline is the L2 K-row gather: see "
+                     "solve_binding_roofline") if dominant == "solve" else
                     "cost bytes = E rows of words present in the corpus + K, K*M writes",
         },
         "solve_binding_roofline": binding,
