@@ -1,1 +1,5 @@
-bash scripts/variants.sh "base:paper_2107_06433_b200/var_base.so:" "r0:paper_2107_06433_b200/var_r0.so:" "r1:paper_2107_06433_b200/var_r1.so:" "r2:paper_2107_06433_b200/var_r2.so:" 2>&1 | grep -E "c2:|c3:|tests"
+mkdir -p gpurun_out
+timeout 600 python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_c3.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none -k regex:"reg_solve|cost_tmap" -s 2 -c 2 -o gpurun_out/prof_c3 python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_c3.log 2>&1; echo ncu_c3_rc=$?
+timeout 600 python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain_c5.log 2>&1 && \
+timeout 1500 ncu --set full --clock-control none -k regex:"cta_solve|cost_tmap" -s 8 -c 2 -o gpurun_out/prof_c5 python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_c5.log 2>&1; echo ncu_c5_rc=$?

@@ -25,7 +25,8 @@ METRICS = {
     "smem_bank_conflicts": ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", 1.0),
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-              "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+              "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+              "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
 
 
 def main(rep, out, note):
@@ -44,6 +45,8 @@ def main(rep, out, note):
             if m not in d or d[m] in ("", "n/a"):
                 continue
             v = float(d[m].replace(",", ""))
+            if v != v:          # NaN (metric not collected for this launch)
+                continue
             unit = u.get(m, "")
             if key.endswith("_bytes"):
                 v *= UNIT_SCALE.get(unit, 1)
