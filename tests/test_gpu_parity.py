@@ -545,3 +545,37 @@ def test_native_plan_graphs_per_query_shape(oracle_lib):
             assert max_rel_err(got.wmd, want) <= RTOL, (rep, k)
             assert set(got.timings) >= {"select", "distances", "iterations", "total"}
             assert got.timings["distances"] > 0 and got.timings["iterations"] > 0
+
+
+def test_query_plan_reset_rides_on_the_cost_build(oracle_lib):
+    """The device-timed path (QueryPlan: cost build whose first thread resets
+    the solve's error record and work counter, then the solve launched with no
+    reset of its own) gives the public API's bits, whatever the counter and
+    the error record held before."""
+    import torch
+
+    from paper_2107_06433_b200 import _lib
+    from paper_2107_06433_b200.device import DeviceCorpus, DeviceEmbeddings, device
+    from paper_2107_06433_b200.solver import QueryPlan
+
+    inst = synth.zipf_instance("c1", n_docs=300)
+    corpus = inst.corpus()
+    cfg = swmd.SolverConfig(lam=10.0, max_iter=15)
+    sel, w = swmd.select_nonzero(inst.query)
+    dev = device()
+    dc = DeviceCorpus.of(corpus, dev)
+    de = DeviceEmbeddings.of(inst.embeddings, dev)
+    plan = QueryPlan(sel, w, dc, de, cfg, swmd.SinkhornWorkspace())
+    for _ in range(2):
+        plan.counter.fill_(123456)            # a stale counter would skip columns
+        plan.err.fill_(7)                     # a stale record would read as an event
+        plan.enqueue_distances()
+        plan.enqueue_solve()
+        torch.cuda.synchronize()
+        got = plan.wmd.cpu().numpy()
+        assert int(plan.err[0]) == _lib.NO_EVENT and int(plan.err[1]) == _lib.NO_EVENT
+        want = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg).wmd
+        assert np.array_equal(got, want)
+    ref = oracle_lib.solve(inst.query, inst.col_ptr, inst.rows, inst.vals, inst.embeddings,
+                           lam=10.0, max_iter=15).wmd
+    assert max_rel_err(got, ref) <= RTOL
