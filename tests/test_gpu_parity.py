@@ -579,3 +579,36 @@ def test_query_plan_reset_rides_on_the_cost_build(oracle_lib):
     ref = oracle_lib.solve(inst.query, inst.col_ptr, inst.rows, inst.vals, inst.embeddings,
                            lam=10.0, max_iter=15).wmd
     assert max_rel_err(got, ref) <= RTOL
+
+
+def test_randomised_instances_match_oracle(oracle_lib):
+    """Seeded sweep over the shapes the persistent kernels specialise on:
+    v_r from 1 to 40 (register-round solve and CTA solve), column lengths
+    from 1 to ~130 (register rounds, slab, past the slab), lambda from 0.5 to
+    30, 1 to 20 iterations; every case within 1e-9 of the oracle and the same
+    top-10."""
+    rng = np.random.default_rng(20261020)
+    for case in range(24):
+        V = int(rng.integers(200, 3000))
+        N = int(rng.integers(1, 150))
+        dim = int(rng.choice([2, 8, 30, 64]))
+        kmin = int(rng.integers(1, 40))
+        kmax = min(V, kmin + int(rng.integers(0, 90)))
+        v_r = int(rng.integers(1, 41))
+        lam = float(rng.choice([0.5, 3.0, 10.0, 30.0]))
+        it = int(rng.integers(1, 21))
+        emb = synth.normal_embeddings(rng, V, dim)
+        cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, kmin, kmax)
+        corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+        q = synth.zipf_query(rng, V, min(v_r, V))
+        cfg = swmd.SolverConfig(lam=lam, max_iter=it)
+        try:
+            want = oracle_lib.solve(q, cp, rows, vals, emb, lam=lam, max_iter=it).wmd
+        except oracle_lib.OracleDegeneracy as exc:
+            with pytest.raises(swmd.DegeneracyError) as got_exc:
+                swmd.sinkhorn_wmd(q, corpus, emb, cfg)
+            assert str(got_exc.value) == str(exc), case
+            continue
+        got = swmd.sinkhorn_wmd(q, corpus, emb, cfg).wmd
+        assert max_rel_err(got, want) <= RTOL, (case, V, N, dim, kmin, kmax, v_r, lam, it)
+        assert _topk_equal(got, want, min(10, N)), case
