@@ -262,6 +262,9 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=dev)
     cfg, n_docs, scaling = _config(args.config, world)
     inst = synth.zipf_instance(cfg, n_docs=n_docs)
+    # a serving table is immutable: read-only, so the resident copy is keyed by
+    # identity (a writeable table is re-hashed in full on every call, device.py)
+    inst.embeddings.flags.writeable = False
     corpus = inst.corpus()
     scfg = swmd.SolverConfig(lam=cfg.lam, max_iter=cfg.max_iter)
     sel, weights = swmd.select_nonzero(inst.query)

@@ -287,6 +287,26 @@ int swmd_topk_f64(const double* values, int64_t n, int32_t k, int64_t index_offs
                   void* stream);
 int64_t swmd_topk_scratch_bytes(int64_t n, int32_t k);
 
+/*
+ * HOST function: claim order of the persistent solve (DeviceCorpus.order) for
+ * `slots` resident warps.  The solve's warps claim columns through one atomic
+ * counter in this order; the reference walks columns in index order
+ * (_jit.py:164-183, deterministic mode) and results do not depend on the
+ * order.  Longest-first when n_cols <= slots or n_cols > max_ratio * slots;
+ * otherwise a MULTIFIT plan (first-fit-decreasing under a binary-searched
+ * capacity) of the per-column time model (register rounds `reg_rounds`,
+ * `slab_rows` shared-memory rows) serialised by planned start time
+ * (paper_2107_06433_b200/schedule.py restates it).  Writes n_cols ids.
+ */
+int swmd_schedule_order(const int64_t* col_ptr, int64_t n_cols, int32_t slots,
+                        int32_t reg_rounds, int32_t slab_rows, int32_t max_ratio,
+                        int32_t* order);
+/* resident warps of the f64 persistent solve for a query of v_r words on the
+ * current device (0 for v_r > 32, whose kernels take columns longest-first),
+ * and its register-round count */
+int swmd_solve_slots_f64(int32_t v_r, int32_t* slots);
+int swmd_solve_reg_rounds_f64(int32_t v_r);
+
 /* Flush helper for benchmarks: writes `bytes` of scratch (> L2 evicts
  * everything) and reads it back, leaving L2 clean (no dirty write-back is
  * charged to the next kernel). */
@@ -296,6 +316,9 @@ int swmd_l2_flush(void* scratch, int64_t bytes, void* stream);
  * array (n elements of itemsize bytes) — the in-place-edit check of the
  * resident embedding-table cache (device.py). */
 int64_t swmd_sample_crc(const void* data, int64_t n, int64_t itemsize);
+/* Host helper: a hash of EVERY byte of a host buffer (`threads` host threads)
+ * — the edit check of a writeable embedding table (device.py). */
+int64_t swmd_content_hash(const void* data, int64_t bytes, int32_t threads);
 
 #ifdef __cplusplus
 }

@@ -71,14 +71,18 @@ _SIGS = {
     "swmd_csr_to_csc_f64": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _P],
     "swmd_csr_to_csc_scratch_bytes": [_I64],
     "swmd_sample_crc": [_P, _I64, _I64],
+    "swmd_content_hash": [_P, _I64, _I32],
     "swmd_topk_scratch_bytes": [_I64, _I32],
     "swmd_plan_create": [_P, _P, _I32],
     "swmd_plan_destroy": [_P],
     "swmd_plan_run": [_P, _P, _I64, _D, _I32, _I32, _P, _P, _P, _P],
+    "swmd_schedule_order": [_P, _I64, _I32, _I32, _I32, _I32, _P],
+    "swmd_solve_slots_f64": [_I32, _P],
+    "swmd_solve_reg_rounds_f64": [_I32],
 }
 _RESTYPE = {"swmd_select_query": ctypes.c_int64, "swmd_topk_scratch_bytes": ctypes.c_int64,
             "swmd_csr_to_csc_scratch_bytes": ctypes.c_int64,
-            "swmd_sample_crc": ctypes.c_int64}
+            "swmd_sample_crc": ctypes.c_int64, "swmd_content_hash": ctypes.c_int64}
 
 EXPORTED = tuple(_SIGS)
 

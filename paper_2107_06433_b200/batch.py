@@ -26,6 +26,7 @@ import torch
 from . import _lib
 from .device import DeviceCorpus, DeviceEmbeddings, device, stream_ptr
 from .kernels import DegeneracyError, select_nonzero, zero_denominator_event
+from .solver import nonpositive_fires
 from .sparse import SparseVector
 
 __all__ = ["solve_batch_f32"]
@@ -52,15 +53,24 @@ def _reset_err(err: torch.Tensor) -> None:
     e[:, 3] = _INT64_MAX
 
 
+# widest query the fp32 solve kernels take (swmd_solve_f32: CTA per column up
+# to 256 words); wider queries of a batch run on the fp64 path
+F32_MAX_V_R = 256
+
+
 def solve_batch_f32(queries, corpus, embeddings, config, ws) -> list:
-    """``sinkhorn_wmd_batch`` semantics in fp32 (see module docstring)."""
-    from .solver import SolverResult
+    """``sinkhorn_wmd_batch`` semantics in fp32 (see module docstring).
+
+    A query wider than F32_MAX_V_R words is solved by the fp64 path instead
+    (its result is at least as accurate), so one wide query never aborts the
+    batch."""
+    from .solver import SolverResult, sinkhorn_wmd
 
     t_start = time.perf_counter()
     n_vocab = corpus.n_rows
     emb_shape = tuple(embeddings.shape)
     results: list = [None] * len(queries)
-    items = []
+    items, wide = [], []
     t0 = time.perf_counter()
     for k, q in enumerate(queries):
         try:
@@ -71,10 +81,24 @@ def solve_batch_f32(queries, corpus, embeddings, config, ws) -> list:
                 raise ValueError(f"shape mismatch: query {q.shape}, embeddings {emb_shape}, "
                                  f"corpus rows {n_vocab}")
             sel, w = select_nonzero(q)
+            if sel.size > F32_MAX_V_R:
+                wide.append((k, q))
+                continue
             items.append((k, sel, w))
         except (ValueError, ArithmeticError) as exc:
             results[k] = exc
     t_select = time.perf_counter() - t0
+    if wide:
+        import dataclasses
+
+        cfg64 = dataclasses.replace(config, precision="f64")
+        emb64 = np.asarray(embeddings, dtype=np.float64) if not hasattr(embeddings, "device") \
+            else embeddings
+        for k, q in wide:
+            try:
+                results[k] = sinkhorn_wmd(q, corpus, emb64, cfg64, workspace=ws)
+            except (ValueError, ArithmeticError) as exc:
+                results[k] = exc
     if not items:
         return results
 
@@ -165,7 +189,7 @@ def _tol_loop(dc, Kp, KMp, rp, v_r, LD, wmd_p, err, n, counter, s, config, dws):
         he = e.cpu().numpy()
         iterations += 1
         cur = nxt
-        if he[0] != _INT64_MAX or he[1] != _INT64_MAX:
+        if he[0] != _INT64_MAX or nonpositive_fires(he):
             return iterations, False
         if float(he[2:3].view(np.float64)[0]) < config.tol:
             converged = True
@@ -178,10 +202,7 @@ def _tol_loop(dc, Kp, KMp, rp, v_r, LD, wmd_p, err, n, counter, s, config, dws):
 def _error_message(he, dc, Kp, KMp, rp, v_r, LD, counter, s, dws):
     zd = zero_denominator_event(he, dc.n_key)
     code_zero = zd[0] if zd is not None else None
-    code_np = int(he[1]) if he[1] != _INT64_MAX else None
-    code_nan = int(he[3]) if he[3] != _INT64_MAX else None
-    if code_np is not None and code_nan is not None and code_nan <= code_np:
-        code_np = None
+    code_np = int(he[1]) if nonpositive_fires(he) else None
     if code_np is not None and (code_zero is None or code_np < code_zero):
         # replay to the failing check with x stored (rare error path)
         N = dc.n_cols

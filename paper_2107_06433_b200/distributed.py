@@ -29,8 +29,8 @@ import torch
 import torch.distributed as dist
 
 from .kernels import DegeneracyError, select_nonzero
-from .solver import (PHASES, DegEvent, LazyTimings, ShardResult, SinkhornWorkspace,
-                     SolverConfig, SolverResult)
+from .solver import (DegEvent, ShardResult, SinkhornWorkspace, SolverConfig, SolverResult,
+                     phase_timings)
 from .sparse import SparseVector, column_blocks
 
 __all__ = ["ShardSolver", "DeviceShardSolver", "shard_bounds", "sinkhorn_wmd_sharded",
@@ -167,13 +167,7 @@ def sinkhorn_wmd_sharded(query, corpus, embeddings, config: SolverConfig,
     for r, p in enumerate(parts):
         a, b = int(bounds[r]), int(bounds[r + 1])
         wmd[a:b] = p[: b - a].cpu().numpy()
-    if isinstance(res.timings, tuple):
-        spans, ev = res.timings
-        timings = LazyTimings({"select": t_select, "total": time.perf_counter() - t_start},
-                              spans, ev)
-    else:
-        timings = {"select": t_select, **res.timings}
-        timings["total"] = time.perf_counter() - t_start
-        timings = {k: timings.get(k, 0.0) for k in PHASES}
+    timings = phase_timings({"select": t_select, "total": time.perf_counter() - t_start},
+                            res.timings)
     return SolverResult(wmd=wmd, iterations_run=res.iterations, converged=res.converged,
                         timings=timings)

@@ -23,8 +23,8 @@ Per-phase times come from CUDA events on the solver's stream.
 
 from __future__ import annotations
 
+import threading
 import time
-from collections.abc import Mapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -182,18 +182,22 @@ def update_u(x: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
 
 # ----------------------------------------------------------------------------------------
 
-_ws_default: SinkhornWorkspace | None = None
+_ws_local = threading.local()
 
 
 def _default_ws() -> SinkhornWorkspace:
-    global _ws_default
-    if _ws_default is None:
-        _ws_default = SinkhornWorkspace()
-    return _ws_default
+    """The implicit workspace of ``workspace=None`` calls: one per host thread,
+    so concurrent solver calls never share staging buffers or a native plan
+    (the reference's contract: concurrent calls on distinct workspaces are
+    safe, SPEC.md:364)."""
+    ws = getattr(_ws_local, "ws", None)
+    if ws is None:
+        ws = _ws_local.ws = SinkhornWorkspace()
+    return ws
 
 
 class _Events:
-    """CUDA events on the solver stream; spans resolve lazily (LazyTimings)."""
+    """CUDA events on the solver stream (per-phase device timings)."""
 
     def __init__(self, enabled: bool):
         self.enabled = enabled
@@ -211,36 +215,18 @@ class _Events:
         return self.ev[a].elapsed_time(self.ev[b]) / 1e3
 
 
-class LazyTimings(Mapping):
-    """The reference's per-phase timings dict (solver.py:131-194).  Device
-    phases are CUDA-event spans resolved on first access, so a solve does not
-    pay for event queries nobody reads."""
+def phase_timings(host: dict, device: dict) -> dict[str, float]:
+    """The reference's per-phase ``timings`` dict (solver.py:131-194): the
+    seven phase keys in order, host phases from ``host``, device phases from
+    ``device`` (seconds; phases fused into another kernel report 0.0)."""
+    d = {**device, **host}
+    return {k: float(d.get(k, 0.0)) for k in PHASES}
 
-    def __init__(self, host: dict, spans: dict, events: _Events):
-        self._host = host
-        self._spans = spans
-        self._events = events
-        self._resolved: dict | None = None
 
-    def _all(self) -> dict:
-        if self._resolved is None:
-            d = dict(self._host)
-            for k, v in self._spans.items():
-                d[k] = self._events.span(*v) if isinstance(v, tuple) else v
-            self._resolved = {k: d[k] for k in PHASES if k in d}
-        return self._resolved
-
-    def __getitem__(self, k):
-        return self._all()[k]
-
-    def __iter__(self):
-        return iter(self._all())
-
-    def __len__(self):
-        return len(self._all())
-
-    def __repr__(self):
-        return repr(self._all())
+def _device_spans(ev: _Events) -> dict[str, float]:
+    """Device phase times once the stream has been synchronised."""
+    return {"distances": ev.span("d0", "d1"), "precompute": 0.0, "init": 0.0,
+            "iterations": ev.span("d1", "i1"), "final": 0.0}
 
 
 def _nonpositive_entry(dc: DeviceCorpus, K, KM, r_dev, v_r: int, ldk: int, t_check: int,
@@ -274,6 +260,16 @@ def _nonpositive_entry(dc: DeviceCorpus, K, KM, r_dev, v_r: int, ldk: int, t_che
 
 def _group(dc: DeviceCorpus, v_r: int) -> int:
     return 32 if dc.mean_len > 64 else 16
+
+
+def nonpositive_fires(he: np.ndarray) -> bool:
+    """Whether the reference's update_u check (solver.py:95-103) fires for the
+    event recorded in err[1]: not when a NaN entry was seen at the same or an
+    earlier check (err[3]) — np.min propagates NaN and ``min(x) <= 0`` is
+    then False."""
+    if he[1] == _lib.NO_EVENT:
+        return False
+    return not (he[3] != _lib.NO_EVENT and int(he[3]) <= int(he[1]))
 
 
 @dataclass(frozen=True)
@@ -419,7 +415,7 @@ class QueryPlan:
             he = host_err.numpy()
             iterations += 1
             cur = nxt
-            fail = he[0] != _lib.NO_EVENT or he[1] != _lib.NO_EVENT
+            fail = he[0] != _lib.NO_EVENT or nonpositive_fires(he)
             delta = float(he[2:3].view(np.float64)[0])
             if allreduce_max is not None:
                 g = allreduce_max(np.array([delta, 1.0 if fail else 0.0]))
@@ -447,10 +443,7 @@ class QueryPlan:
         dc = self.dc
         zd = zero_denominator_event(he, dc.n_key)
         code_zero = zd[0] if zd is not None else None
-        code_nonpos = int(he[1]) if he[1] != _lib.NO_EVENT else None
-        code_nan = int(he[3]) if he[3] != _lib.NO_EVENT else None
-        if code_nonpos is not None and code_nan is not None and code_nan <= code_nonpos:
-            code_nonpos = None   # np.min propagates NaN: the reference's check does not fire
+        code_nonpos = int(he[1]) if nonpositive_fires(he) else None
         if code_nonpos is not None and (code_zero is None or code_nonpos < code_zero):
             val, flat = _nonpositive_entry(dc, self.K, self.KM, self.r_dev, self.v_r, self.ldk,
                                            code_nonpos // 2, self.dws)
@@ -488,9 +481,7 @@ def solve_on_device(sel: np.ndarray | None, weights: np.ndarray | None, dc: Devi
         ev.mark("i1")
     wmd_host, he = plan.readback()
     event = plan.decode_event(he)
-    spans = {"distances": ("d0", "d1"), "precompute": 0.0, "init": 0.0,
-             "iterations": ("d1", "i1"), "final": 0.0}
-    return ShardResult(wmd_host, iterations, converged, (spans, ev), event)
+    return ShardResult(wmd_host, iterations, converged, _device_spans(ev), event)
 
 
 def _stage_query(query, n_vocab: int, ws: SinkhornWorkspace) -> int:
@@ -642,9 +633,9 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
             raise _lib.NativeError(f"swmd_plan_run: CUDA error {rc}")
         if rc == 0 and plan.err[0] == _lib.NO_EVENT and plan.err[1] == _lib.NO_EVENT:
             t = plan.times
-            timings = {"select": float(t[2]) / 1e3, "distances": float(t[0]) / 1e3,
-                       "precompute": 0.0, "init": 0.0, "iterations": float(t[1]) / 1e3,
-                       "final": 0.0, "total": time.perf_counter() - t_start}
+            timings = phase_timings(
+                {"select": float(t[2]) / 1e3, "total": time.perf_counter() - t_start},
+                {"distances": float(t[0]) / 1e3, "iterations": float(t[1]) / 1e3})
             return SolverResult(wmd=wmd, iterations_run=config.max_iter, converged=False,
                                 timings=timings)
         # rc == -4 (outside the native fast path) or a degeneracy to decode:
@@ -658,10 +649,9 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
     res = solve_on_device(None, None, dc, de, config, ws, staged_v_r=v_r)
     if res.event is not None:
         raise DegeneracyError(res.event.message)
-    spans, ev = res.timings
     host = {"select": t_select, "total": time.perf_counter() - t_start}
     return SolverResult(wmd=res.wmd, iterations_run=res.iterations, converged=res.converged,
-                        timings=LazyTimings(host, spans, ev))
+                        timings=phase_timings(host, res.timings))
 
 
 @dataclass(frozen=True)
@@ -674,7 +664,7 @@ class TopKResult:
     wmd: np.ndarray
     iterations_run: int
     converged: bool
-    timings: Mapping
+    timings: dict[str, float]
 
 
 def sinkhorn_wmd_topk(query, corpus, embeddings, config: SolverConfig, k: int,
@@ -727,12 +717,10 @@ def sinkhorn_wmd_topk(query, corpus, embeddings, config: SolverConfig, k: int,
     event = plan.decode_event(hn[2 * k:].copy())
     if event is not None:
         raise DegeneracyError(event.message)
-    spans = {"distances": ("d0", "d1"), "precompute": 0.0, "init": 0.0,
-             "iterations": ("d1", "i1"), "final": 0.0}
     host_t = {"select": t_select, "total": time.perf_counter() - t_start}
     return TopKResult(indices=hn[:k].copy(), wmd=hn[k: 2 * k].view(np.float64).copy(),
                       iterations_run=iterations, converged=converged,
-                      timings=LazyTimings(host_t, spans, ev))
+                      timings=phase_timings(host_t, _device_spans(ev)))
 
 
 def sinkhorn_wmd_batch(queries, corpus, embeddings, config: SolverConfig,

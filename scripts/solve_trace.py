@@ -54,3 +54,8 @@ for name in sys.argv[1:] or ["c2"]:
     print("  columns in flight at 10..90 % of the span:", busy)
     per_sm = np.bincount(sm, minlength=148)
     print(f"  columns per SM: min {per_sm.min()} max {per_sm.max()}")
+    edges = np.linspace(0, (t1.max() - base) / 1e3, 41)
+    print("  in flight (40 buckets):", [int(((st < b) & (en > b)).sum()) for b in edges[1:-1]])
+    out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    np.save(os.path.join(out, f"strace_{name}.npy"), np.stack([ln, sm, t0 - base, t1 - base], 1))

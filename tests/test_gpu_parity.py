@@ -358,6 +358,16 @@ def test_sparse_vector_query_and_embedding_cache():
     b = swmd.sinkhorn_wmd(inst.query, corpus, emb, cfg).wmd
     c = swmd.sinkhorn_wmd(inst.query, corpus, emb.copy(), cfg).wmd
     assert not np.array_equal(a, b) and np.array_equal(b, c)
+    # ... including a single-row edit of a row the corpus uses
+    row = int(inst.rows[inst.col_ptr[3]])
+    emb[row] *= 0.5
+    d = swmd.sinkhorn_wmd(inst.query, corpus, emb, cfg).wmd
+    e = swmd.sinkhorn_wmd(inst.query, corpus, emb.copy(), cfg).wmd
+    assert not np.array_equal(b, d) and np.array_equal(d, e)
+    # a read-only table is cached by identity (its buffer cannot change)
+    ro = emb.copy()
+    ro.flags.writeable = False
+    assert np.array_equal(swmd.sinkhorn_wmd(inst.query, corpus, ro, cfg).wmd, e)
 
 
 def test_torch_cuda_embeddings():

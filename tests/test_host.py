@@ -197,3 +197,23 @@ def test_generator_is_deterministic_and_thread_independent():
     y = synth.zipf_corpus_csc(rng2, 1000, 300, 5, 20, chunk=40)
     for p, q in zip(x, y):
         assert np.array_equal(p, q)
+
+
+def test_embedding_fingerprint_sees_one_element_edits():
+    """a writeable table is hashed in full, so editing one element
+    (anywhere) changes its cache key; a read-only table is sampled."""
+    from paper_2107_06433_b200.device import _fingerprint, _read_only
+
+    E = np.random.default_rng(0).standard_normal((20_000, 30))
+    f0 = _fingerprint(E)
+    old = E[5, 7]
+    E[5, 7] = old + 1.0
+    f1 = _fingerprint(E)
+    E[5, 7] = old
+    assert f1 != f0 and _fingerprint(E) == f0
+    v = E.view()
+    v.flags.writeable = False
+    assert not _read_only(v)                    # its base is still writeable
+    R = E.copy()
+    R.flags.writeable = False
+    assert _read_only(R)
