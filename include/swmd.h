@@ -93,7 +93,7 @@ int swmd_cost_build_f64(const double* E, int64_t V, int32_t dim, int64_t ldE,
  * even): row r of E_c is vocabulary row row_ids[r] (row_ids NULL: identity).
  * E (row stride ldE) supplies the query vectors, norms are per vocabulary row.
  * Streams E_c through TMA tensor copies (cp.async.bulk.tensor, 128-byte
- * swizzle, 16-stage mbarrier ring) into the FP64 tensor pipe (DMMA).
+ * swizzle, 4-stage mbarrier ring of 32 KB boxes) into the FP64 tensor pipe (DMMA).
  */
 int swmd_cost_build_compact_f64(const double* E, int64_t ldE, const double* E_c, int64_t n_c,
                                 int32_t dim, int64_t ldEc, const int32_t* row_ids,

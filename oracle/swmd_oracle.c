@@ -277,6 +277,34 @@ static int update_u(const double* x, double* u, int64_t n, int64_t* flat, double
  * distances, precompute, iterations, final, total (omp_get_wtime).
  * Returns ORACLE_OK or an error kind with errpos / errval filled.
  */
+/* max |a - b| over n entries with numpy's NaN propagation (np.max returns
+ * NaN when any entry is NaN; solver.py:180) */
+static double max_abs_diff(const double* a, const double* b, int64_t n) {
+    double m = 0.0;
+    int nan = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        const double d = fabs(a[k] - b[k]);
+        if (d != d) nan = 1;
+        else if (d > m) m = d;
+    }
+    return nan ? NAN : m;
+}
+
+/*
+ * oracle_solve with SolverConfig.tol (solver.py:170-183): tol < 0 means None.
+ * After iteration t, delta = max|x - x_prev| is written to deltas[t] and the
+ * loop stops when delta < tol; *iterations / *converged receive the
+ * reference's iterations_run / converged.
+ */
+int oracle_solve_tol(const double* vecs, int64_t n_rows, int64_t dim,
+                     const int64_t* sel, const double* weights, int64_t vr,
+                     const int64_t* col_ptr, const int32_t* rows, const double* vals,
+                     int64_t n_cols, double lam, int64_t max_iter, double tol, int64_t nblocks,
+                     double* cost, double* kernel, double* kor, double* kcost,
+                     double* x, double* x_prev, double* u, double* wmd,
+                     int64_t* errpos, double* errval, double* timings,
+                     int64_t* iterations, int32_t* converged, double* deltas);
+
 int oracle_solve(const double* vecs, int64_t n_rows, int64_t dim,
                  const int64_t* sel, const double* weights, int64_t vr,
                  const int64_t* col_ptr, const int32_t* rows, const double* vals,
@@ -284,6 +312,21 @@ int oracle_solve(const double* vecs, int64_t n_rows, int64_t dim,
                  double* cost, double* kernel, double* kor, double* kcost,
                  double* x, double* x_prev, double* u, double* wmd,
                  int64_t* errpos, double* errval, double* timings) {
+    int64_t it = 0;
+    int32_t conv = 0;
+    return oracle_solve_tol(vecs, n_rows, dim, sel, weights, vr, col_ptr, rows, vals, n_cols,
+                            lam, max_iter, -1.0, nblocks, cost, kernel, kor, kcost, x, x_prev,
+                            u, wmd, errpos, errval, timings, &it, &conv, NULL);
+}
+
+int oracle_solve_tol(const double* vecs, int64_t n_rows, int64_t dim,
+                     const int64_t* sel, const double* weights, int64_t vr,
+                     const int64_t* col_ptr, const int32_t* rows, const double* vals,
+                     int64_t n_cols, double lam, int64_t max_iter, double tol, int64_t nblocks,
+                     double* cost, double* kernel, double* kor, double* kcost,
+                     double* x, double* x_prev, double* u, double* wmd,
+                     int64_t* errpos, double* errval, double* timings,
+                     int64_t* iterations, int32_t* converged, double* deltas) {
     double t_start = 0, t0 = 0;
 #ifdef _OPENMP
     t_start = omp_get_wtime();
@@ -305,6 +348,8 @@ int oracle_solve(const double* vecs, int64_t n_rows, int64_t dim,
     int64_t n = n_cols * vr;
     for (int64_t k = 0; k < n; ++k) x[k] = 1.0 / (double)vr;
     int rc = ORACLE_OK;
+    *iterations = 0;
+    *converged = 0;
     for (int64_t it = 0; it < max_iter; ++it) {
         rc = update_u(x, u, n, &errpos[0], errval);
         if (rc) { errpos[1] = -1; goto done; }
@@ -313,6 +358,12 @@ int oracle_solve(const double* vecs, int64_t n_rows, int64_t dim,
         oracle_fused_iter_columns(col_ptr, rows, vals, bounds, nblocks, kernel, kor,
                                   vr, u, x, errpos);
         if (errpos[0] >= 0) { rc = ORACLE_ZERO_DENOM; goto done; }
+        *iterations = it + 1;
+        if (tol >= 0.0) {
+            const double delta = max_abs_diff(x, x_prev, n);
+            if (deltas) deltas[it] = delta;
+            if (delta < tol) { *converged = 1; break; }
+        }
     }
 #ifdef _OPENMP
     timings[2] = omp_get_wtime() - t0; t0 = omp_get_wtime();

@@ -70,3 +70,60 @@ def column_subset(corpus, cols):
         new_cp.append(new_cp[-1] + (b - a))
     return CsrMatrix.from_csc(corpus.n_rows, len(cols), np.array(new_cp),
                               np.concatenate(r_out), np.concatenate(v_out))
+
+
+def tol_case(g, n: int):
+    """Inputs and parameters of tol golden case n (tests/golden/tol.npz):
+    (query, CsrMatrix corpus, embeddings, lam, max_iter, tol)."""
+    from paper_2107_06433_b200 import synth
+
+    spec = str(g[f"t{n}_spec"])
+    lam, max_iter, tol = (float(v) for v in g[f"t{n}_params"])
+    kind, arg = spec.split(":")
+    if kind == "small":
+        q, corpus, emb = small_instance(golden("small"), int(arg))
+    else:
+        inst = synth.zipf_instance(kind, n_docs=int(arg) or None)
+        q, corpus, emb = inst.query, inst.corpus(), inst.embeddings
+    return q, corpus, emb, lam, int(max_iter), tol
+
+
+def check_topk(got, ref_idx, ref_val, k: int, rtol: float = 1e-9, ref_full=None):
+    """Top-k parity (north_star: identical top-k document indices).
+
+    ``ref_idx`` / ``ref_val``: the reference's top-(k+1) (np.argsort stable)
+    indices and values.  The stable top-k of ``got`` must equal the
+    reference's, except at a rank p where the document placed there is a
+    near-tie (within ``rtol``) of the reference's value at rank p — the only
+    legitimate flip.  A document from outside the reference's
+    top-(k+1) may only enter when the reference's rank-p and rank-(k+1)
+    values are themselves within ``rtol`` (a boundary tie).  ``ref_full``
+    (the whole reference vector) makes the check exact.  Returns the flips
+    (rank, got doc, reference doc) for reporting; raises AssertionError
+    otherwise."""
+    got = np.asarray(got)
+    top = np.argsort(got, kind="stable")[:k]
+    ref_idx = np.asarray(ref_idx)[: k + 1]
+    ref_val = np.asarray(ref_val)[: k + 1]
+    if np.array_equal(top, ref_idx[:k]):
+        return []
+    pos = {int(d): p for p, d in enumerate(ref_idx)}
+    flips = []
+    for p in range(k):
+        d = int(top[p])
+        if d == int(ref_idx[p]):
+            continue
+        rv = ref_val[p]
+        if ref_full is not None:
+            v = float(ref_full[d])
+        elif d in pos:
+            v = float(ref_val[pos[d]])
+        else:
+            v = float(got[d])
+            assert abs(ref_val[k] - rv) <= rtol * max(abs(rv), abs(ref_val[k])), (
+                f"rank {p}: doc {d} from outside the reference top-{k + 1} without a boundary tie")
+        assert abs(v - rv) <= rtol * max(abs(v), abs(rv)), (
+            f"rank {p}: doc {d} (reference value {v!r}) where the reference has doc "
+            f"{int(ref_idx[p])} ({rv!r})")
+        flips.append((p, d, int(ref_idx[p])))
+    return flips

@@ -14,8 +14,15 @@ Outputs (committed):
   c1.npz, c2.npz - full ``wmd`` of the reference solver on the seeded
                Zipf configs (paper_2107_06433_b200.synth), plus sha256
                fingerprints of the generated inputs.
-  c3.npz, c5.npz - reference top-100 (stable argsort), sum, and a strided
-               sample of ``wmd`` (the full vectors are too big to commit).
+  c3.npz, c5.npz - reference top-100 (stable argsort), the top-101 indices
+               and values (the (k+1)-th decides boundary near-ties), sum, and
+               a strided sample of ``wmd`` (the full vectors are too big to
+               commit).
+  c4.npz      - 64 fp64 reference solves of the c4 instance: top-11, sums,
+               samples.
+  tol.npz     - the reference's ``tol`` early exit (solver.py:170-183):
+               iterations_run, converged, wmd and the per-iteration
+               max|x - x_prev| of its loop, on c1/c2-shaped and small cases.
 
 The reference runs with SolverConfig(deterministic=True, workers=os.cpu_count()),
 which is bitwise equal to its serial mode (test_acceptance.py:126-151).
@@ -118,6 +125,8 @@ def make_config(name: str, full: bool):
         fp_embeddings=np.array(fingerprint(inst.embeddings)),
         top100=order[:100],
         top100_wmd=wmd[order[:100]],
+        top101=order[:101],
+        top101_wmd=wmd[order[:101]],
         wmd_sum=np.array(float(np.sum(wmd))),
         sample_stride=np.array(max(1, wmd.size // 1000)),
         sample=wmd[:: max(1, wmd.size // 1000)],
@@ -150,8 +159,8 @@ def make_c4():
     for q in inst.queries:
         res = sinkwmd.sinkhorn_wmd(q, corpus, E64, scfg)
         order = np.argsort(res.wmd, kind="stable")
-        tops.append(order[:10])
-        topv.append(res.wmd[order[:10]])
+        tops.append(order[:11])
+        topv.append(res.wmd[order[:11]])
         sums.append(float(np.sum(res.wmd)))
         samples.append(res.wmd[::stride])
         vrs.append(int(np.count_nonzero(q)))
@@ -160,18 +169,83 @@ def make_c4():
         nnz=np.array(inst.nnz),
         fp_corpus=np.array(fingerprint(inst.col_ptr, inst.rows, inst.vals)),
         fp_embeddings=np.array(fingerprint(inst.embeddings)),
-        top10=np.array(tops), top10_wmd=np.array(topv), wmd_sum=np.array(sums),
+        top10=np.array(tops)[:, :10], top10_wmd=np.array(topv)[:, :10],
+        top11=np.array(tops), top11_wmd=np.array(topv), wmd_sum=np.array(sums),
         sample_stride=np.array(stride), sample=np.array(samples), v_r=np.array(vrs))
     print(f"c4.npz: nnz={inst.nnz} queries={len(inst.queries)} v_r={vrs[:8]}... "
           f"{time.time() - t0:.1f}s")
 
 
+def _ref_tol_run(query, corpus, emb, lam, max_iter, tol):
+    """The reference solver's result plus the max|x - x_prev| of every
+    iteration, recomputed by the reference's own pieces in its loop order
+    (solver.py:160-183: update_u, fused_iteration, max-norm check)."""
+    scfg = sinkwmd.SolverConfig(lam=lam, max_iter=max_iter, tol=tol,
+                                workers=os.cpu_count() or 1, deterministic=True)
+    res = sinkwmd.sinkhorn_wmd(query, corpus, emb, scfg)
+    sel, weights = sinkwmd.select_nonzero(query)
+    mats = sinkwmd.precompute(sinkwmd.euclidean_rows(emb, sel), weights, lam)
+    x = np.full((corpus.n_cols, sel.size), 1.0 / sel.size)
+    deltas = []
+    for _ in range(res.iterations_run):
+        u = sinkwmd.solver.update_u(x)
+        xn = np.zeros_like(x)
+        sinkwmd.fused_iteration(corpus, mats, u, xn, workers=os.cpu_count() or 1,
+                                deterministic=True)
+        deltas.append(float(np.max(np.abs(xn - x))))
+        x = xn
+    return res, np.array(deltas)
+
+
+def make_tol():
+    """Pinned tol semantics: c1 and c2-shaped Zipf instances at lam=1 (the
+    reference's own tol test uses lam=1, test_solver.py:112-129), a run
+    that exhausts max_iter, and small random instances."""
+    out = {}
+    cases = []
+    for name, n_docs, lam, max_iter, tol in [("c1", None, 1.0, 500, 1e-9),
+                                             ("c2", 1000, 1.0, 500, 1e-9),
+                                             ("c2", 1000, 1.0, 6, 1e-12),
+                                             ("c1", None, 10.0, 200, 1e-7)]:
+        inst = synth.zipf_instance(name, n_docs=n_docs)
+        rp, ci, v = synth.csc_to_csr(inst.n_vocab, inst.n_docs, inst.col_ptr, inst.rows, inst.vals)
+        corpus = CsrMatrix(inst.n_vocab, inst.n_docs, rp, ci, v)
+        res, deltas = _ref_tol_run(inst.query, corpus, inst.embeddings, lam, max_iter, tol)
+        cases.append((f"{name}:{n_docs or 0}", lam, max_iter, tol, res, deltas))
+    for k in range(6):
+        seed = 1000 + k
+        rng = np.random.default_rng(seed)
+        n_vocab = int(rng.integers(8, 65))
+        n_docs = int(rng.integers(2, 17))
+        v_r = int(rng.integers(1, min(8, n_vocab) + 1))
+        dim = int(rng.integers(2, 9))
+        inst = random_instance(seed, n_vocab=n_vocab, n_docs=n_docs, v_r=v_r, dim=dim,
+                               density=0.25)
+        res, deltas = _ref_tol_run(inst.query, inst.corpus, inst.embeddings, 1.0, 500, 1e-9)
+        cases.append((f"small:{k}", 1.0, 500, 1e-9, res, deltas))
+    for n, (spec, lam, max_iter, tol, res, deltas) in enumerate(cases):
+        p = f"t{n}_"
+        out[p + "spec"] = np.array(spec)
+        out[p + "params"] = np.array([lam, max_iter, tol])
+        out[p + "iterations"] = np.array(res.iterations_run)
+        out[p + "converged"] = np.array(res.converged)
+        out[p + "wmd"] = res.wmd
+        out[p + "deltas"] = deltas
+        print(f"tol case {spec} lam={lam} max_iter={max_iter} tol={tol}: "
+              f"{res.iterations_run} iterations, converged={res.converged}, "
+              f"last deltas {deltas[-3:]}")
+    out["n_cases"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(HERE, "tol.npz"), **out)
+
+
 def main(argv):
     sinkwmd.kernels.warmup()
-    which = argv or ["small", "c1", "c2", "c3", "c4", "c5"]
+    which = argv or ["small", "c1", "c2", "c3", "c4", "c5", "tol"]
     for w in which:
         if w == "small":
             make_small()
+        elif w == "tol":
+            make_tol()
         elif w == "c4":
             make_c4()
         else:

@@ -110,3 +110,40 @@ def test_c4_oracle_pinned_on_four_queries(oracle_lib):
         res = oracle_lib.solve(inst.queries[k], inst.col_ptr, inst.rows, inst.vals, E64,
                                lam=10.0, max_iter=20)
         assert np.array_equal(res.wmd[::stride], g["sample"][k]), k
+
+
+def test_oracle_tol_path_pinned(oracle_lib):
+    """The oracle's tol early exit equals the reference's (tests/golden/tol.npz,
+    solver.py:170-183): iterations_run, converged, every max|dx| and wmd bitwise."""
+    from conftest import tol_case
+
+    g = golden("tol")
+    for n in range(int(g["n_cases"])):
+        q, corpus, emb, lam, max_iter, tol = tol_case(g, n)
+        cp, rows, _, vals = corpus.csc_index()
+        res = oracle_lib.solve(q, cp, rows, vals, emb, lam=lam, max_iter=max_iter, tol=tol,
+                               blocks=3)
+        assert res.iterations_run == int(g[f"t{n}_iterations"]), n
+        assert res.converged == bool(g[f"t{n}_converged"]), n
+        assert np.array_equal(res.deltas, g[f"t{n}_deltas"]), n
+        assert np.array_equal(res.wmd, g[f"t{n}_wmd"]), n
+
+
+def test_check_topk_rules():
+    """The strict top-k checker the GPU parity tests use."""
+    from conftest import check_topk
+
+    ref = np.array([0.5, 0.1, 0.3, 0.2, 0.9, 0.30000000000000004])
+    idx = np.argsort(ref, kind="stable")
+    assert check_topk(ref, idx, ref[idx], 3) == []
+    # swapping the near-tie at ranks 2/3 (docs 2 and 5) is legitimate at k=3 and k=4
+    got = ref.copy()
+    got[5] = 0.3 - 1e-16
+    assert check_topk(got, idx, ref[idx], 3, ref_full=ref) == [(2, 5, 2)]
+    # a real reordering is not
+    bad = ref.copy()
+    bad[0] = 0.15
+    with pytest.raises(AssertionError):
+        check_topk(bad, idx, ref[idx], 3, ref_full=ref)
+    with pytest.raises(AssertionError):                 # outside doc, no boundary tie
+        check_topk(bad, idx[:4], ref[idx][:4], 3)
