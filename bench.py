@@ -245,6 +245,199 @@ def _transpose_times(inst, dev) -> dict:
             "note": "device = pageable CSR upload + swmd_csr_to_csc_f64 + col_ptr readback"}
 
 
+def _fusion_compare(sel, weights, dc, de, scfg, flush_buf, reps: int) -> dict:
+    """Fused persistent solve vs the unfused comparator (SDDMM -> w in HBM ->
+    SpMM per iteration; baseline.unfused_sparse_wmd, reference baseline.py:
+    67-131, timed against the fused solver in reference bench.py:49-89) on the
+    same resident K: the iteration + final phases only, CUDA events, L2
+    flushed before each solve.  The unfused launches are replayed from a CUDA
+    graph so host launch overhead does not count against it."""
+    import torch
+
+    from paper_2107_06433_b200 import _lib
+    from paper_2107_06433_b200.baseline import UnfusedPlan
+    from paper_2107_06433_b200.solver import QueryPlan, SinkhornWorkspace
+
+    side = torch.cuda.Stream(device=dc.device)
+    out = {}
+    with torch.cuda.stream(side):
+        s = side.cuda_stream
+        fused = QueryPlan(sel, weights, dc, de, scfg, SinkhornWorkspace())
+        unf = UnfusedPlan(sel, weights, dc, de, scfg, SinkhornWorkspace())
+        fused.enqueue_distances()
+        unf.enqueue_distances()
+        fused.enqueue_solve()
+        unf.enqueue_solve()
+        side.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            unf.enqueue_solve()
+        graph.replay()
+        side.synchronize()
+        a = fused.wmd.cpu().numpy()
+        b = unf.wmd.cpu().numpy()
+        out["max_rel_diff"] = float(np.max(np.abs(a - b) / np.maximum(np.abs(a), 1e-300)))
+        times = {"fused": [], "unfused": []}
+        for _ in range(reps):
+            for name in ("fused", "unfused"):
+                _lib.call("swmd_l2_flush", flush_buf.data_ptr(), flush_buf.numel(), s)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(side)
+                if name == "fused":
+                    fused.enqueue_solve()
+                else:
+                    graph.replay()
+                e1.record(side)
+                times[name].append((e0, e1))
+        side.synchronize()
+    f_ms = float(np.median([x.elapsed_time(y) for x, y in times["fused"]]))
+    u_ms = float(np.median([x.elapsed_time(y) for x, y in times["unfused"]]))
+    it = scfg.max_iter
+    out.update({
+        "fused_solve_ms": f_ms, "unfused_solve_ms": u_ms, "fusion_speedup": u_ms / f_ms,
+        "fused_launches_per_solve": 1, "unfused_launches_per_solve": 2 * it + 1,
+        "unfused_w_bytes_per_iter": int(2 * 8 * dc.nnz),
+        "reps": reps,
+        "note": "iterations + final pass on resident K (cost build excluded, same for both); "
+                "unfused = swmd_unfused_iterate_f64 (SDDMM storing w, SpMM reading it) per "
+                "iteration + swmd_unfused_final_f64, graph-replayed; medians, L2 flushed "
+                "before each solve; the paper reports 1.15-2.22x on CPUs",
+    })
+    return out
+
+
+def _c3_strong(args, world: int, rank: int, dev, flush_buf) -> dict | None:
+    """The north-star scaling workload (BASELINE configs[2], "c3": N=1M docs,
+    ~45M nnz) strong-scaled over the ``world`` ranks: column_blocks shards
+    (reference sparse.py:261-276), K built on every rank, the solve writing
+    into the rank's slot of ONE all_gather_into_tensor per step.  Device time
+    per step = CUDA events around (cost build, solve, gather), max over ranks.
+    With world > 1, rank 0 also times the whole c3 solve alone on its GPU, so
+    the line carries the 1 -> N efficiency of this run.  Rank 0 gets the dict."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_06433_b200 as swmd
+    from paper_2107_06433_b200 import _lib, synth
+    from paper_2107_06433_b200.distributed import _TAIL, DeviceShardSolver, shard_bounds
+    from paper_2107_06433_b200.distributed import sinkhorn_wmd_sharded
+    from paper_2107_06433_b200.solver import QueryPlan
+
+    cfg = synth.CONFIGS["c3"]
+    inst = synth.zipf_instance(cfg)
+    inst.embeddings.flags.writeable = False
+    corpus = inst.corpus()
+    scfg = swmd.SolverConfig(lam=cfg.lam, max_iter=cfg.max_iter)
+    sel, weights = swmd.select_nonzero(inst.query)
+    bounds = shard_bounds(corpus, world)
+    c0, c1 = int(bounds[rank]), int(bounds[rank + 1])
+    width = int(np.max(np.diff(bounds)))
+    solver = DeviceShardSolver(corpus, inst.embeddings, dev=dev)
+    dc = solver.block(c0, c1)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    slot = torch.zeros(width + _TAIL, dtype=torch.float64, device=dev)
+    gathered = torch.empty(world * (width + _TAIL), dtype=torch.float64, device=dev)
+    plan = QueryPlan(sel, weights, dc, solver.de, scfg, solver.ws)
+    plan.wmd = slot[: c1 - c0]
+    plan.err = slot[width: width + 4].view(torch.int64)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record()
+        plan.enqueue_distances()
+        plan.enqueue_solve()
+        if ev is not None:
+            ev[1].record()
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, slot)
+        if ev is not None:
+            ev[2].record()
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = args.c3_steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(steps):
+        _lib.call("swmd_l2_flush", flush_buf.data_ptr(), flush_buf.numel(), s)
+        step(evs[k])
+    torch.cuda.synchronize()
+    tot = float(sum(e[0].elapsed_time(e[2]) for e in evs))
+    comp = float(sum(e[0].elapsed_time(e[1]) for e in evs))
+    gat = float(sum(e[1].elapsed_time(e[2]) for e in evs))
+    t = torch.tensor([tot, comp, gat], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot, comp, gat = (float(v) for v in t.cpu())
+
+    # e2e through the public sharded API (query in, all N distances out on every rank)
+    for _ in range(2):
+        res = sinkhorn_wmd_sharded(inst.query, corpus, inst.embeddings, scfg, solver=solver) \
+            if world > 1 else swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, scfg,
+                                                workspace=solver.ws)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = sinkhorn_wmd_sharded(inst.query, corpus, inst.embeddings, scfg, solver=solver) \
+            if world > 1 else swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, scfg,
+                                                workspace=solver.ws)
+    e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e.item())
+
+    one_ms = None
+    if world > 1:
+        dist.barrier()
+        if rank == 0:   # the same workload on this GPU alone
+            full = DeviceShardSolver(corpus, inst.embeddings, dev=dev)
+            dfull = full.block(0, corpus.n_cols)
+            p1 = QueryPlan(sel, weights, dfull, full.de, scfg, full.ws)
+            for _ in range(2):
+                p1.enqueue_distances()
+                p1.enqueue_solve()
+            torch.cuda.synchronize()
+            ev1 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+            for k in range(steps):
+                _lib.call("swmd_l2_flush", flush_buf.data_ptr(), flush_buf.numel(), s)
+                ev1[k][0].record()
+                p1.enqueue_distances()
+                p1.enqueue_solve()
+                ev1[k][1].record()
+            torch.cuda.synchronize()
+            one_ms = float(np.mean([a.elapsed_time(b) for a, b in ev1]))
+            ok = np.array_equal(p1.wmd.cpu().numpy(), res.wmd)
+            assert ok, "c3 sharded result differs from the single-GPU solve"
+            del p1, full, dfull
+        dist.barrier()
+    if rank != 0:
+        return None
+    ms = tot / steps
+    out = {
+        "workload": f"c3: V={cfg.n_vocab} N={inst.n_docs} docs, nnz={inst.nnz}, v_r={sel.size}, "
+                    f"lam={cfg.lam}, max_iter={cfg.max_iter}; column_blocks over {world} rank(s)",
+        "n_gpus": world, "steps": steps,
+        "ms_per_step": ms, "compute_ms": comp / steps, "gather_ms": gat / steps,
+        "value": inst.nnz * cfg.max_iter / (ms / 1e3), "unit": UNIT,
+        "e2e": {"ms_per_step": 1e3 * e2e_s / steps,
+                "value": inst.nnz * cfg.max_iter * steps / e2e_s, "unit": UNIT,
+                "note": "public sinkhorn_wmd_sharded() (N>1) / sinkhorn_wmd() (N=1), "
+                        "corpus and E resident; max over ranks"},
+        "shard_nnz_max": int(np.max(np.diff(corpus.csc_compact()[0][bounds]))),
+        "l2": "flushed before every step",
+        "note": "device time per step = max over ranks of (cost build + solve + "
+                "all_gather_into_tensor of the distance slots)",
+    }
+    if one_ms is not None:
+        out["one_gpu_ms_per_step"] = one_ms
+        out["efficiency"] = one_ms / (world * ms)
+    return out
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -349,6 +542,9 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     assert np.array_equal(res.wmd[c0:c1], wmd_dev.cpu().numpy()), "device-timed result drifted"
+    c3_block = None
+    if args.c3 and args.config == "c2":
+        c3_block = _c3_strong(args, world, rank, dev, flush_buf)
 
     if rank != 0:
         if world > 1:
@@ -450,8 +646,13 @@ def run_b200(args):
         "gpu_launches": int(launches),
         "clocks": clock_info,
     }
+    if c3_block is not None:
+        line["c3_strong"] = c3_block
     if world == 1:
         line["corpus_transpose"] = _transpose_times(inst, dev)
+        if not args.no_fusion and int(sel.size) <= 64:
+            line["fusion"] = _fusion_compare(sel, weights, dc, de, scfg, flush_buf,
+                                             reps=50 if args.config in ("c1", "c2") else 5)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline(inst, cfg)
     print(json.dumps(line), flush=True)
@@ -524,6 +725,11 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-flush", dest="flush", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3", dest="c3", action="store_false",
+                    help="skip the c3 strong-scaling block of the c2 line")
+    ap.add_argument("--c3-steps", type=int, default=10)
+    ap.add_argument("--no-fusion", action="store_true",
+                    help="skip the fused-vs-unfused comparison (1 GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -216,6 +216,32 @@ int swmd_spmm_f64(const int64_t* col_ptr, const int32_t* rows, const int64_t* po
                   const double* w, int64_t n_cols, const double* kernel_over_r,
                   int32_t v_r, int64_t ldk, double* x, void* stream);
 
+/* Unfused comparator, one Sinkhorn iteration t (baseline.unfused_sparse_wmd,
+ * baseline.py:67-131): an SDDMM launch that applies update_u to x_in while
+ * loading each column's row (event code 2t; x_in == NULL means x = 1/v_r,
+ * init_x) and stores w[q] = vals[q] / (K[rows[q],:] . u[j,:]) for every
+ * nonzero q in CSC order in HBM (zero denominator: w = 0, code 2t+1), then an
+ * SpMM launch that reads w back and writes x_out[j,a] = (sum_q K[rows[q],a]
+ * w[q]) / r[a] and records max |x_out - x_in| in err[2] (the tol test,
+ * solver.py:179-183).  Rows are padded: ldk == ldx == swmd_unfused_row_width
+ * (v_r) (pad columns of K zero).  v_r <= 64; SWMD_EVR otherwise. */
+int swmd_unfused_row_width(int32_t v_r);
+int swmd_unfused_iterate_f64(const int64_t* col_ptr, const int32_t* rows,
+                             const double* vals, int64_t n_cols, const double* kernel,
+                             const double* r, int32_t v_r, int64_t ldk,
+                             const double* x_in, double* x_out, int64_t ldx, double* w,
+                             int32_t t, int64_t key_off, int64_t n_key, int64_t* err,
+                             void* stream);
+
+/* Unfused comparator, final pass after t_final iterations: update_u on x_in
+ * (code 2*t_final) and wmd[j] = sum_q (vals[q] / (K[i,:] . u)) (KM[i,:] . u)
+ * (code 2*t_final+1), i.e. kernels.fused_final (kernels.py:313-354). */
+int swmd_unfused_final_f64(const int64_t* col_ptr, const int32_t* rows,
+                           const double* vals, int64_t n_cols, const double* kernel,
+                           const double* kernel_cost, int32_t v_r, int64_t ldk,
+                           const double* x_in, int64_t ldx, double* wmd, int32_t t_final,
+                           int64_t key_off, int64_t n_key, int64_t* err, void* stream);
+
 /* u = 1/x elementwise with the update_u check (solver.py:95-103): records
  * `code` in err[1] if any entry <= 0 and in err[3] if any entry is NaN. */
 int swmd_update_u_f64(const double* x, double* u, int64_t n, int32_t code,

@@ -60,6 +60,11 @@ _SIGS = {
     "swmd_sddmm_f64": [_P, _P, _P, _P, _I64, _P, _I32, _I64, _P, _P, _I64, _P, _P],
     "swmd_spmm_f64": [_P, _P, _P, _P, _I64, _P, _I32, _I64, _P, _P],
     "swmd_update_u_f64": [_P, _P, _I64, _I32, _P, _P],
+    "swmd_unfused_row_width": [_I32],
+    "swmd_unfused_iterate_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _I32,
+                                 _I64, _I64, _P, _P],
+    "swmd_unfused_final_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _I64, _P, _I32, _I64,
+                               _I64, _P, _P],
     "swmd_l2_flush": [_P, _I64, _P],
     "swmd_select_query": [_P, _I64, _P, _I64],
     "swmd_row_norms_f32": [_P, _I64, _I32, _I64, _P, _P],

@@ -164,19 +164,28 @@ class DeviceCorpus:
     _foreign: dict[int, dict] = {}
 
     @classmethod
+    def _store(cls, corpus) -> dict:
+        """The per-corpus cache of resident copies: on the corpus object when it
+        has a slot for it (this package's CsrMatrix), else keyed by id and
+        dropped when the corpus is collected."""
+        store = getattr(corpus, "_device_cache", None)
+        if isinstance(store, dict):
+            return store
+        store = cls._foreign.get(id(corpus))
+        if store is None:
+            store = {}
+            cls._foreign[id(corpus)] = store
+            try:
+                weakref.finalize(corpus, cls._foreign.pop, id(corpus), None)
+            except TypeError:
+                pass
+        return store
+
+    @classmethod
     def of(cls, corpus, dev: torch.device | None = None) -> "DeviceCorpus":
         dev = dev or device()
         key = (dev.type, dev.index)
-        store = getattr(corpus, "_device_cache", None)
-        if not isinstance(store, dict):
-            store = cls._foreign.get(id(corpus))
-            if store is None:
-                store = {}
-                cls._foreign[id(corpus)] = store
-                try:
-                    weakref.finalize(corpus, cls._foreign.pop, id(corpus), None)
-                except TypeError:
-                    pass
+        store = cls._store(corpus)
         dc = store.get(key)
         if dc is None and _row_major_only(corpus):
             dc = cls.from_csr(corpus.n_rows, corpus.n_cols, corpus.row_ptr, corpus.col_idx,
@@ -191,6 +200,25 @@ class DeviceCorpus:
             dc = cls(corpus.n_rows, cp, rows, vals, dev, pos=pos_host)
             if pos_host is None and hasattr(corpus, "csc_index"):
                 dc._pos_host_fn = corpus.csc_index
+            store[key] = dc
+        return dc
+
+    @classmethod
+    def block_of(cls, corpus, dev: torch.device, c0: int, c1: int) -> "DeviceCorpus":
+        """Columns [c0, c1) of ``corpus`` resident on ``dev`` (a shard of the
+        multi-GPU split), cached on the corpus like ``of``."""
+        if (c0, c1) == (0, corpus.n_cols):
+            return cls.of(corpus, dev)
+        store = cls._store(corpus)
+        key = (dev.type, dev.index, int(c0), int(c1))
+        dc = store.get(key)
+        if dc is None:
+            if hasattr(corpus, "csc_compact"):
+                cp, rows, vals = corpus.csc_compact()
+            else:
+                cp, rows, _, vals = corpus.csc_index()
+            dc = cls(corpus.n_rows, cp[c0: c1 + 1], rows, vals, dev, col_offset=c0,
+                     n_key=corpus.n_cols)
             store[key] = dc
         return dc
 

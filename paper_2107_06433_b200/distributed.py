@@ -8,9 +8,14 @@ that never split a column.  Columns are independent (test_acceptance.py:
 embedding table (and hence K) replicated, and there is no data-path
 collective until the end:
 
-* one all-gather of the per-rank distance blocks (padded to equal length);
-* one small all-gather of each rank's earliest degeneracy event, so every
-  rank raises the same error the single-process solve would;
+* one ``all_gather_into_tensor`` of equal per-rank slots — the distance
+  block (padded to the widest block), the block's raw device error record,
+  the iteration count and the converged flag.  On the GPU the solve writes
+  its distances and error record straight into the slot, so nothing crosses
+  PCIe before the gather and the result comes back in one device->host copy;
+* only if some rank recorded a degeneracy, one more small all-gather of each
+  rank's decoded earliest event, so every rank raises the same error the
+  single-process solve would;
 * with ``tol`` set, one 2-double all-reduce(MAX) per iteration (the global
   max-norm change and an any-failed flag), keeping ``converged`` and
   ``iterations_run`` global (solver.py:179-183).
@@ -52,11 +57,17 @@ def shard_bounds(corpus, world: int) -> np.ndarray:
 
 
 class DeviceShardSolver:
-    """The GPU shard solver: this rank's column block resident on its device."""
+    """The GPU shard solver: this rank's column block resident on its device.
+
+    ``__call__`` is the ShardSolver protocol (host result).  ``solve_into``
+    is the device path ``sinkhorn_wmd_sharded`` uses: the solve writes its
+    distances straight into the rank's slot of the gather buffer and the raw
+    error record next to them, so nothing crosses PCIe before the gather.
+    """
 
     def __init__(self, corpus, embeddings, workspace: SinkhornWorkspace | None = None,
                  dev: torch.device | None = None):
-        from .device import DeviceCorpus, DeviceEmbeddings, device
+        from .device import DeviceEmbeddings, device
 
         self.corpus = corpus
         self.dev = dev or device()
@@ -64,24 +75,50 @@ class DeviceShardSolver:
         self.ws = workspace or SinkhornWorkspace()
         self._blocks: dict[tuple[int, int], object] = {}
 
-    def __call__(self, sel, weights, c0, c1, config, allreduce_max):
+    def block(self, c0: int, c1: int):
+        """This rank's column block, uploaded once (only its columns)."""
         from .device import DeviceCorpus
-        from .solver import solve_on_device
 
         blk = self._blocks.get((c0, c1))
         if blk is None:
-            if (c0, c1) == (0, self.corpus.n_cols):
-                blk = DeviceCorpus.of(self.corpus, self.dev)
-            else:   # upload only this rank's column block
-                if hasattr(self.corpus, "csc_compact"):
-                    cp, rows, vals = self.corpus.csc_compact()
-                else:
-                    cp, rows, _, vals = self.corpus.csc_index()
-                blk = DeviceCorpus(self.corpus.n_rows, cp[c0: c1 + 1], rows, vals, self.dev,
-                                   col_offset=c0, n_key=self.corpus.n_cols)
+            blk = DeviceCorpus.block_of(self.corpus, self.dev, c0, c1)
             self._blocks[(c0, c1)] = blk
-        return solve_on_device(sel, weights, blk, self.de, config, self.ws,
+        return blk
+
+    def __call__(self, sel, weights, c0, c1, config, allreduce_max):
+        from .solver import solve_on_device
+
+        return solve_on_device(sel, weights, self.block(c0, c1), self.de, config, self.ws,
                                allreduce_max=allreduce_max)
+
+    def solve_into(self, sel, weights, c0, c1, config, allreduce_max, slot: torch.Tensor):
+        """Solve the block with ``slot[:c1-c0]`` (float64, on this device) as
+        the distance buffer and the error record written to
+        ``slot[width:width+4]`` (int64 bits).  Returns (iterations,
+        converged, decode) — ``decode(err_words)`` yields the block's DegEvent."""
+        from .solver import QueryPlan, _device_spans, _Events
+
+        dc = self.block(c0, c1)
+        plan = QueryPlan(sel, weights, dc, self.de, config, self.ws)
+        width = slot.numel() - _TAIL
+        plan.wmd = slot[: c1 - c0]
+        plan.err = slot[width: width + 4].view(torch.int64)
+        ev = _Events(True)
+        ev.mark("d0")
+        plan.enqueue_distances()
+        ev.mark("d1")
+        if config.tol is None:
+            plan.enqueue_solve()
+            iterations, converged = config.max_iter, False
+        else:
+            iterations, converged = plan.run_tol(allreduce_max)
+        ev.mark("i1")
+        return iterations, converged, plan.decode_event, lambda: _device_spans(ev)
+
+
+# per-rank gather slot: distances (padded to the widest block) | the block's
+# error record (4 int64 words, swmd.h) | iterations run | converged
+_TAIL = 6
 
 
 def merge_events(events: list[DegEvent | None]) -> DegEvent | None:
@@ -128,46 +165,70 @@ def sinkhorn_wmd_sharded(query, corpus, embeddings, config: SolverConfig,
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         return t.cpu().numpy()
 
-    res = solver(sel, weights, c0, c1, config, allreduce_max if config.tol is not None else None)
+    arm = allreduce_max if config.tol is not None else None
 
-    # one gather of the distance blocks (padded to the largest block)
+    # ONE all-gather of equal slots: [distances | error record | iterations | converged]
     width = int(np.max(np.diff(bounds))) if world else 0
-    mine = torch.zeros(width + 1, dtype=torch.float64)
-    mine[: c1 - c0] = torch.from_numpy(np.ascontiguousarray(res.wmd[: c1 - c0]))
-    # the last slot carries this rank's iteration count (equal on all ranks)
-    mine[width] = float(res.iterations)
-    mine = mine.to(cdev)
-    parts = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(parts, mine, group=group)
+    slot = torch.zeros(width + _TAIL, dtype=torch.float64, device=cdev)
+    if isinstance(solver, DeviceShardSolver) and cdev.type == "cuda":
+        iterations, converged, decode, spans = solver.solve_into(sel, weights, c0, c1, config,
+                                                                 arm, slot)
+    else:
+        res = solver(sel, weights, c0, c1, config, arm)
+        host = np.zeros(width + _TAIL, dtype=np.float64)
+        host[: c1 - c0] = res.wmd[: c1 - c0]
+        words = host[width: width + 4].view(np.int64)
+        words[:] = _NO_EVENT
+        if res.event is not None:
+            words[0] = 0                      # "this block has an event"
+        iterations, converged = res.iterations, res.converged
+        decode = lambda _words, ev=res.event: ev   # noqa: E731
+        spans = lambda t=res.timings: t   # noqa: E731
+        slot.copy_(torch.from_numpy(host))
+    slot[width + 4] = float(iterations)
+    slot[width + 5] = 1.0 if converged else 0.0
+    gathered = torch.empty(world * (width + _TAIL), dtype=torch.float64, device=cdev)
+    dist.all_gather_into_tensor(gathered, slot, group=group)
+    allv = gathered.cpu().numpy().reshape(world, width + _TAIL)
+    words_all = allv[:, width: width + 4].copy().view(np.int64)
 
-    # one gather of the degeneracy events
-    ev = res.event
-    enc = np.full(4, np.inf)
-    if ev is not None:
-        enc[:] = [ev.code, *[float(k) for k in ev.key], rank]
-    etens = torch.from_numpy(enc).to(cdev)
-    eparts = [torch.empty_like(etens) for _ in range(world)]
-    dist.all_gather(eparts, etens, group=group)
-    evs = []
-    for p in eparts:
-        e = p.cpu().numpy()
-        if np.isfinite(e[0]):
-            evs.append(e)
-    if evs:
-        best = min(evs, key=lambda e: (e[0], e[1], e[2]))
-        # the owning rank's message text; every rank reconstructs it
-        code, k0, k1 = int(best[0]), best[1], best[2]
-        if code % 2 == 0:
-            msg = f"nonpositive iterate entry {float(k0)} at flat index {int(k1)}"
-        else:
-            msg = f"zero denominator at nonzero ({int(k0)}, {int(k1)})"
-        raise DegeneracyError(msg)
+    if any(_has_event(w) for w in words_all):
+        # rare path: every rank decodes its own block's event, one more gather
+        own = words_all[rank]
+        ev = decode(own) if _has_event(own) else None
+        enc = np.full(4, np.inf)
+        if ev is not None:
+            enc[:] = [ev.code, *[float(k) for k in ev.key], rank]
+        etens = torch.from_numpy(enc).to(cdev)
+        eparts = torch.empty(4 * world, dtype=torch.float64, device=cdev)
+        dist.all_gather_into_tensor(eparts, etens, group=group)
+        evs = [e for e in eparts.cpu().numpy().reshape(world, 4) if np.isfinite(e[0])]
+        if evs:
+            best = min(evs, key=lambda e: (e[0], e[1], e[2]))
+            # the owning rank's message text; every rank reconstructs it
+            code, k0, k1 = int(best[0]), best[1], best[2]
+            if code % 2 == 0:
+                msg = f"nonpositive iterate entry {float(k0)} at flat index {int(k1)}"
+            else:
+                msg = f"zero denominator at nonzero ({int(k0)}, {int(k1)})"
+            raise DegeneracyError(msg)
 
     wmd = np.empty(corpus.n_cols, dtype=np.float64)
-    for r, p in enumerate(parts):
+    for r in range(world):
         a, b = int(bounds[r]), int(bounds[r + 1])
-        wmd[a:b] = p[: b - a].cpu().numpy()
+        wmd[a:b] = allv[r, : b - a]
     timings = phase_timings({"select": t_select, "total": time.perf_counter() - t_start},
-                            res.timings)
-    return SolverResult(wmd=wmd, iterations_run=res.iterations, converged=res.converged,
-                        timings=timings)
+                            spans())
+    return SolverResult(wmd=wmd, iterations_run=int(allv[0, width + 4]),
+                        converged=bool(allv[0, width + 5]), timings=timings)
+
+
+_NO_EVENT = (1 << 63) - 1
+
+
+def _has_event(words: np.ndarray) -> bool:
+    """Whether an error record holds an event the reference would raise
+    (a zero denominator, or a nonpositive iterate not masked by NaN)."""
+    from .solver import nonpositive_fires
+
+    return int(words[0]) != _NO_EVENT or nonpositive_fires(words)

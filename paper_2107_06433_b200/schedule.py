@@ -36,11 +36,13 @@ __all__ = ["column_cost", "balanced_order", "longest_first", "plan_makespan"]
 # together), then one serial step per 16-nonzero slab / L2 round.  The
 # constants are the A/B winner on the B200 (profiles/r02_summary.md): the
 # realised span is not monotone in model accuracy — a fit to the c2
-# SOLVE_TRACE timeline (0.41/0.22/0.36) planned a 2 us longer span
-COST_FIXED = 0.55
-COST_REG = 0.14
-COST_SLAB = 0.33
-COST_L2 = 0.45
+# SOLVE_TRACE timeline (0.41/0.22/0.36) planned a 2 us longer span.  With the
+# shuffle reduction (REG_SHRED) the fixed per-pass part shrank and the flat
+# model (0.3/0.3/0.3) won: 55.6 us vs 56.9 us for the round-1 constants
+COST_FIXED = 0.3
+COST_REG = 0.3
+COST_SLAB = 0.3
+COST_L2 = 0.4
 
 
 def column_cost(lens: np.ndarray, reg_rounds: int = 2, slab_rows: int = 48) -> np.ndarray:

@@ -51,6 +51,7 @@ __all__ = [
     "update_u",
     "sinkhorn_wmd",
     "sinkhorn_wmd_batch",
+    "sinkhorn_wmd_devices",
     "solve_on_device",
     "DegEvent",
     "ShardResult",
@@ -305,7 +306,7 @@ class QueryPlan:
 
     def __init__(self, sel: np.ndarray | None, weights: np.ndarray | None, dc: DeviceCorpus,
                  de: DeviceEmbeddings, config: SolverConfig, ws: SinkhornWorkspace,
-                 staged_v_r: int | None = None):
+                 staged_v_r: int | None = None, ldk: int | None = None):
         self.dc, self.de, self.config, self.ws = dc, de, config, ws
         self.dev = dc.device
         self._stream = stream_ptr(self.dev)
@@ -323,6 +324,8 @@ class QueryPlan:
         # K row stride = v_r rounded up to 4 (zero pad columns): 16-byte rows that
         # the fast v_r <= 32 kernel reads as whole pairs without masking
         self.ldk = ((v_r + 3) // 4) * 4 if v_r <= 32 else v_r + (v_r & 1)
+        if ldk is not None:   # a caller-chosen padded width (the unfused comparator)
+            self.ldk = int(ldk)
         V, N = dc.n_rows, dc.n_cols
         qdev = dws.flat("qdev", 2 * v_r, torch.int64)
         qdev.copy_(stage[: 2 * v_r], non_blocking=True)
@@ -396,27 +399,44 @@ class QueryPlan:
         self.launches += 1
         self._solve(0, self.config.max_iter, None, None, self.wmd)
 
+    # tol path, split so several plans (devices) can run it in lockstep
+    def tol_begin(self) -> None:
+        n = self.dc.n_cols * self.v_r
+        self._tol_bufs = (self.dws.flat("x_a", n), self.dws.flat("x_b", n))
+        self._tol_host = self.ws.pinned("err_host", _lib.ERR_WORDS, torch.int64)
+        self._armed = False
+        _lib.call("swmd_err_reset", self.err.data_ptr(), self.stream)
+        self._cur = None
+
+    def tol_launch(self, t: int) -> None:
+        """Iteration t with x stored; the error record (max|dx| in err[2]) is
+        copied to pinned host memory behind it."""
+        nxt = self._tol_bufs[t % 2]
+        self.err[2].zero_()
+        self._solve(t, t + 1, self._cur, nxt, None)
+        self._tol_host.copy_(self.err, non_blocking=True)
+        self._cur = nxt
+
+    def tol_read(self) -> tuple[bool, float]:
+        """(failed, max|dx|) of the last launched iteration (synchronises)."""
+        torch.cuda.synchronize(self.dev)
+        he = self._tol_host.numpy()
+        fail = he[0] != _lib.NO_EVENT or nonpositive_fires(he)
+        return bool(fail), float(he[2:3].view(np.float64)[0])
+
+    def tol_final(self, iterations: int) -> None:
+        self._solve(iterations, iterations, self._cur, None, self.wmd)
+
     def run_tol(self, allreduce_max=None) -> tuple[int, bool]:
         """tol set: one launch per iteration, max|dx| read back after each
         (solver.py:170-183), then the final pass.  Returns (iterations, converged)."""
         cfg = self.config
-        n = self.dc.n_cols * self.v_r
-        bufs = (self.dws.flat("x_a", n), self.dws.flat("x_b", n))
-        host_err = self.ws.pinned("err_host", _lib.ERR_WORDS, torch.int64)
-        self._armed = False
-        _lib.call("swmd_err_reset", self.err.data_ptr(), self.stream)
-        cur, iterations, converged, failed = None, 0, False, False
+        self.tol_begin()
+        iterations, converged, failed = 0, False, False
         for t in range(cfg.max_iter):
-            nxt = bufs[t % 2]
-            self.err[2].zero_()
-            self._solve(t, t + 1, cur, nxt, None)
-            host_err.copy_(self.err)
-            torch.cuda.current_stream(self.dev).synchronize()
-            he = host_err.numpy()
+            self.tol_launch(t)
+            fail, delta = self.tol_read()
             iterations += 1
-            cur = nxt
-            fail = he[0] != _lib.NO_EVENT or nonpositive_fires(he)
-            delta = float(he[2:3].view(np.float64)[0])
             if allreduce_max is not None:
                 g = allreduce_max(np.array([delta, 1.0 if fail else 0.0]))
                 delta, fail = float(g[0]), bool(g[1] > 0)
@@ -427,7 +447,7 @@ class QueryPlan:
                 converged = True
                 break
         if not failed:
-            self._solve(iterations, iterations, cur, None, self.wmd)
+            self.tol_final(iterations)
         return iterations, converged
 
     def readback(self) -> tuple[np.ndarray, np.ndarray]:
@@ -609,6 +629,11 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
             f"shape mismatch: query {query.shape}, embeddings "
             f"{emb_shape}, corpus rows {n_vocab}")
     ws = workspace if workspace is not None else _default_ws()
+    if config.workers > 1 and config.precision == "f64" and corpus.n_cols > 1 and cuda_ok():
+        n_dev = min(config.workers, torch.cuda.device_count())
+        if n_dev > 1:   # workers -> GPUs: one column block per device
+            devs = [torch.device("cuda", k) for k in range(n_dev)]
+            return sinkhorn_wmd_devices(query, corpus, embeddings, config, devs, ws, t_start)
     if config.precision == "f32":
         from .batch import solve_batch_f32
 
@@ -652,6 +677,89 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
     host = {"select": t_select, "total": time.perf_counter() - t_start}
     return SolverResult(wmd=res.wmd, iterations_run=res.iterations, converged=res.converged,
                         timings=phase_timings(host, res.timings))
+
+
+def sinkhorn_wmd_devices(query, corpus, embeddings, config: SolverConfig,
+                         devices: list[torch.device], workspace: SinkhornWorkspace | None = None,
+                         t_start: float | None = None) -> SolverResult:
+    """``sinkhorn_wmd`` with the document columns split over ``devices`` in
+    this one process: the reference's ``workers`` (solver.py:35, threads over
+    nnz-balanced column blocks, sparse.py:261-276) become GPUs.  Each device
+    gets a contiguous column_blocks shard (uploaded once, cached on the
+    corpus), builds K itself and runs the persistent solve on its own stream;
+    the host enqueues every device before it waits on any, then reads each
+    block back.  With ``tol`` the devices step in lockstep and share one
+    global max|dx| (solver.py:179-183).  A device may appear more than once
+    (one block per entry).  Results are bitwise those of the one-launch solve."""
+    from .sparse import column_blocks
+
+    t_start = time.perf_counter() if t_start is None else t_start
+    ws = workspace if workspace is not None else _default_ws()
+    t0 = time.perf_counter()
+    sel, weights = select_nonzero(query)
+    t_select = time.perf_counter() - t0
+    col_ptr = corpus.csc_compact()[0] if hasattr(corpus, "csc_compact") else corpus.csc_index()[0]
+    bounds = column_blocks(col_ptr, len(devices))
+    shard_ws = ws.__dict__.setdefault("_shard_ws", {})
+    plans, evs = [], []
+    for k, dev in enumerate(devices):
+        c0, c1 = int(bounds[k]), int(bounds[k + 1])
+        if c1 <= c0:
+            continue
+        with torch.cuda.device(dev):
+            sws = shard_ws.setdefault(k, SinkhornWorkspace())
+            dc = DeviceCorpus.block_of(corpus, dev, c0, c1)
+            de = DeviceEmbeddings.of(embeddings, dev)
+            plan = QueryPlan(sel, weights, dc, de, config, sws)
+            ev = _Events(True)
+            ev.mark("d0")
+            plan.enqueue_distances()
+            ev.mark("d1")
+            if config.tol is None:
+                plan.enqueue_solve()
+                ev.mark("i1")
+            plans.append((c0, c1, plan))
+            evs.append(ev)
+    iterations, converged, failed = config.max_iter, False, False
+    if config.tol is not None:
+        for _, _, plan in plans:
+            with torch.cuda.device(plan.dev):
+                plan.tol_begin()
+        iterations = 0
+        for t in range(config.max_iter):
+            for _, _, plan in plans:
+                with torch.cuda.device(plan.dev):
+                    plan.tol_launch(t)
+            reads = [plan.tol_read() for _, _, plan in plans]
+            iterations += 1
+            if any(f for f, _ in reads):
+                failed = True
+                break
+            if max(d for _, d in reads) < config.tol:   # NaN never converges (np.max)
+                converged = True
+                break
+        for (_, _, plan), ev in zip(plans, evs):
+            with torch.cuda.device(plan.dev):
+                if not failed:
+                    plan.tol_final(iterations)
+                ev.mark("i1")
+    wmd = np.empty(corpus.n_cols, dtype=np.float64)
+    events = []
+    for c0, c1, plan in plans:
+        with torch.cuda.device(plan.dev):
+            part, he = plan.readback()
+            events.append(plan.decode_event(he))
+        wmd[c0:c1] = part
+    from .distributed import merge_events
+
+    ev0 = merge_events(events)
+    if ev0 is not None:
+        raise DegeneracyError(ev0.message)
+    spans = [_device_spans(e) for e in evs]
+    dev_t = {k: max(sp[k] for sp in spans) for k in spans[0]} if spans else {}
+    return SolverResult(wmd=wmd, iterations_run=iterations, converged=converged,
+                        timings=phase_timings({"select": t_select,
+                                               "total": time.perf_counter() - t_start}, dev_t))
 
 
 @dataclass(frozen=True)
