@@ -54,6 +54,35 @@ def main(rep, out, note):
             elif key == "duration_us":
                 v *= UNIT_SCALE.get(unit, 1)
             ent[key] = v
+        # every pipe-utilisation counter the capture holds (tensor/DMMA, FMA, FP64, ALU, ...)
+        pipes = {}
+        for h, v in d.items():
+            m = re.match(r"sm__pipe_(\w+?)_cycles_active\.avg\.pct_of_peak_sustained_active$", h)
+            if m and v not in ("", "n/a"):
+                try:
+                    pipes[m.group(1)] = round(float(v.replace(",", "")), 2)
+                except ValueError:
+                    pass
+            m = re.match(r"sm__inst_executed_pipe_(\w+?)\.avg\.pct_of_peak_sustained_active$", h)
+            if m and v not in ("", "n/a"):
+                try:
+                    pipes["inst_" + m.group(1)] = round(float(v.replace(",", "")), 2)
+                except ValueError:
+                    pass
+        if pipes:
+            ent["pipes_pct_of_peak_active"] = dict(sorted(pipes.items(), key=lambda kv: -kv[1]))
+        for key, m in (("issue_active_pct", "sm__issue_active.avg.pct_of_peak_sustained_active"),
+                       ("l1tex_throughput_pct", "l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                       ("lts_bytes", "lts__t_bytes.sum"),
+                       ("sm_throughput_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed")):
+            if m in d and d[m] not in ("", "n/a"):
+                try:
+                    v = float(d[m].replace(",", ""))
+                    if key == "lts_bytes":
+                        v = int(v * UNIT_SCALE.get(u.get(m, ""), 1))
+                    ent[key] = v
+                except ValueError:
+                    pass
         stalls = []
         for h, v in d.items():
             if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
