@@ -735,11 +735,12 @@ def run_batch_f32(args):
     cost_ms = 1e3 * cost_s / args.steps
     fp32_peak = 148 * 128 * 2 * 1.965e3          # GFLOP/s: FFMA lanes x 2 x max SM clock
     probes = {}
-    try:
-        with open(os.path.join(REPO, "profiles", "r01_probes.json")) as f:
-            probes = json.load(f)
-    except (OSError, ValueError):
-        pass
+    for pf in ("r01_probes.json", "r02_probes.json"):
+        try:
+            with open(os.path.join(REPO, "profiles", pf)) as f:
+                probes.update(json.load(f))
+        except (OSError, ValueError):
+            pass
     fp32_peak = float(probes.get("fp32_ffma_tflops", fp32_peak / 1e3)) * 1e3
     solve_flops = (T + 1) * flops
     achieved = solve_flops / (solve_ms / 1e3) / 1e9
