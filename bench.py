@@ -480,6 +480,10 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's own init log (rank count, transport, NVLS) on stderr, so the
+        # communicator the run used can be checked next to the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     cfg, n_docs, scaling = _config(args.config, world)
     inst = synth.zipf_instance(cfg, n_docs=n_docs)
@@ -696,6 +700,7 @@ def run_batch_f32(args):
     import torch
 
     import paper_2107_06433_b200 as swmd
+    from paper_2107_06433_b200 import batch as batch_mod
     from paper_2107_06433_b200 import synth
 
     world, rank, local = _dist_env()
@@ -761,11 +766,14 @@ def run_batch_f32(args):
                 "d2h_bytes_per_step": int(Q * (inst.n_docs * 4 + 32)),
                 "ms_per_step": 1e3 * wall / args.steps,
                 "note": "public sinkhorn_wmd_batch(precision='f32'); corpus, E resident"},
-        "gpu_launches": int((2 + Q) * args.steps),
+        "gpu_launches": int(batch_mod.last_launches * args.steps),
         "clocks": clock_info,
         "kernels": {"cost_build_ms": cost_ms, "solves_ms": solve_ms,
                     "cost_build": "gram32_kernel (one launch for the batch)",
-                    "solve": f"reg_solve<float> / cta_solve<float>, one persistent launch per query"},
+                    "solve": "reg_solve_mq<float>: one persistent launch per group of up to 4 "
+                             "queries of one padded width, each claimed column solved for every "
+                             "query of the group (CSC read once per group)",
+                    "solve_launches_per_batch": int(batch_mod.last_launches - 2)},
         "roofline": {
             "bound": "fp32", "kernel": "swmd_solve_f32 (persistent fused loop, all queries)",
             "achieved": achieved, "peak": fp32_peak, "unit": "GFLOP/s", "frac": achieved / fp32_peak,

@@ -216,6 +216,23 @@ int swmd_spmm_f64(const int64_t* col_ptr, const int32_t* rows, const int64_t* po
                   const double* w, int64_t n_cols, const double* kernel_over_r,
                   int32_t v_r, int64_t ldk, double* x, void* stream);
 
+/* Multi-query fp32 solve of one group of nq <= 4 queries with the same padded
+ * width (v_rs[q] rounded up to 8, v_rs[q] <= 64) on one corpus: the whole
+ * loop (max_iter iterations + the final pass, tol unset) in ONE persistent
+ * launch that claims columns and solves each claimed column for every query
+ * of the group in turn, so the column's CSC entries are read from HBM once
+ * per group.  Per query q: kernels[q] / kernel_costs[q] (row stride ldk,
+ * 16-byte aligned blocks of the batch K), weights[q] (v_rs[q] floats),
+ * wmds[q] (n_cols floats), errs[q] (the 4-word error record, reset by the
+ * caller).  Pointer arrays are host arrays of device pointers.  Replaces the
+ * per-query loop of sinkhorn_wmd_batch (solver.py:204-223). */
+int swmd_solve_group_f32(const int64_t* col_ptr, const int32_t* rows, const double* vals,
+                         int64_t n_cols, const int32_t* order, int32_t nq,
+                         const float* const* kernels, const float* const* kernel_costs,
+                         const float* const* weights, const int32_t* v_rs, int64_t ldk,
+                         int32_t max_iter, float* const* wmds, int64_t* const* errs,
+                         int64_t col_key_offset, int64_t n_key, int32_t* counter, void* stream);
+
 /* Unfused comparator, one Sinkhorn iteration t (baseline.unfused_sparse_wmd,
  * baseline.py:67-131): an SDDMM launch that applies update_u to x_in while
  * loading each column's row (event code 2t; x_in == NULL means x = 1/v_r,

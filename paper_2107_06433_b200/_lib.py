@@ -72,6 +72,8 @@ _SIGS = {
                                   _I64, _P, _P, _P],
     "swmd_solve_f32": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
                        _I64, _I64, _I32, _P, _P, _P],
+    "swmd_solve_group_f32": [_P, _P, _P, _I64, _P, _I32, _P, _P, _P, _P, _I64, _I32, _P, _P,
+                             _I64, _I64, _P, _P],
     "swmd_topk_f64": [_P, _I64, _I32, _I64, _P, _P, _P, _I64, _P],
     "swmd_csr_to_csc_f64": [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _P],
     "swmd_csr_to_csc_scratch_bytes": [_I64],

@@ -13,6 +13,10 @@ work the B200 way:
 * each query's K block is a 16-byte-aligned column range of that matrix,
   zero-padded to v_r rounded to 8, and the fp32 solve kernel reads it in
   place (row stride = the batch width);
+* queries of one padded width are solved GROUP (4) at a time in one
+  persistent launch (``swmd_solve_group_f32``): a claimed column is solved
+  for each query of the group in turn, so its CSC entries are fetched from
+  HBM once per group instead of once per query;
 * one device->host copy returns every query's distances and error record.
 """
 
@@ -31,6 +35,8 @@ from .sparse import SparseVector
 
 __all__ = ["solve_batch_f32"]
 
+last_launches = 0   # kernels the last tol-unset batch launched (bench.py reports it)
+
 _INT64_MAX = (1 << 63) - 1
 
 
@@ -43,6 +49,28 @@ def _solve32(dc, K_ptr, KM_ptr, r_ptr, v_r, LD, t0, t1, x_in, x_out, wmd_ptr, er
               dc.n_cols, dc.order.data_ptr(), K_ptr, KM_ptr, r_ptr, v_r, LD, t0, t1,
               x_in, x_out, wmd_ptr, dc.col_offset, dc.n_key, dc.max_len, err_ptr,
               counter.data_ptr(), s)
+
+
+# queries per group launch (swmd_solve_group_f32 takes up to 4): their K blocks
+# (4 x ~14 MB at c4) stay L2-resident together while a column is solved for each
+GROUP = 4
+
+
+def _solve_group32(dc, members, LD, max_iter, counter, s):
+    import ctypes
+
+    nq = len(members)
+    P = ctypes.c_void_p * nq
+    kp = P(*[m[0] for m in members])
+    kmp = P(*[m[1] for m in members])
+    rp = P(*[m[2] for m in members])
+    wp = P(*[m[3] for m in members])
+    ep = P(*[m[4] for m in members])
+    vr = (ctypes.c_int32 * nq)(*[m[5] for m in members])
+    _lib.call("swmd_solve_group_f32", dc.col_ptr.data_ptr(), dc.rows.data_ptr(), dc.vals.data_ptr(),
+              dc.n_cols, dc.order.data_ptr(), nq, ctypes.addressof(kp), ctypes.addressof(kmp),
+              ctypes.addressof(rp), ctypes.addressof(vr), LD, max_iter, ctypes.addressof(wp),
+              ctypes.addressof(ep), dc.col_offset, dc.n_key, counter.data_ptr(), s)
 
 
 def _reset_err(err: torch.Tensor) -> None:
@@ -143,21 +171,45 @@ def solve_batch_f32(queries, corpus, embeddings, config, ws) -> list:
     _reset_err(err)
     iters = [config.max_iter] * nq
     conv = [False] * nq
+    ptrs = []
     for n, ((k, sel, _), o, wo) in enumerate(zip(items, offs, woffs)):
-        Kp = K.data_ptr() + 4 * o
-        KMp = KM.data_ptr() + 4 * o
-        rp = w_d.data_ptr() + 4 * wo
-        wmd_p = out.data_ptr() + 4 * n * N
-        err_p = err.data_ptr() + 8 * n * _lib.ERR_WORDS
-        if config.tol is None:
-            _solve32(dc, Kp, KMp, rp, sel.size, LD, 0, config.max_iter, None, None, wmd_p,
-                     err_p, counter, s)
-        else:
-            iters[n], conv[n] = _tol_loop(dc, Kp, KMp, rp, sel.size, LD, wmd_p, err, n,
+        ptrs.append((K.data_ptr() + 4 * o, KM.data_ptr() + 4 * o, w_d.data_ptr() + 4 * wo,
+                     out.data_ptr() + 4 * n * N, err.data_ptr() + 8 * n * _lib.ERR_WORDS,
+                     int(sel.size)))
+    launches = 2   # the Gram build + the error-record reset
+    if config.tol is None:
+        # queries of one padded width share a launch, GROUP at a time: each
+        # claimed column is solved for every query of the group in turn
+        by_width: dict[int, list[int]] = {}
+        for n, p in enumerate(ptrs):
+            if p[5] <= 64:
+                by_width.setdefault(_block_width(p[5]), []).append(n)
+            else:
+                Kp, KMp, rp, wmd_p, err_p, v_r = p
+                _solve32(dc, Kp, KMp, rp, v_r, LD, 0, config.max_iter, None, None, wmd_p,
+                         err_p, counter, s)
+                launches += 1
+        for members in by_width.values():
+            for g0 in range(0, len(members), GROUP):
+                _solve_group32(dc, [ptrs[n] for n in members[g0: g0 + GROUP]], LD,
+                               config.max_iter, counter, s)
+                launches += 1
+        global last_launches
+        last_launches = launches
+    else:
+        for n, (Kp, KMp, rp, wmd_p, err_p, v_r) in enumerate(ptrs):
+            iters[n], conv[n] = _tol_loop(dc, Kp, KMp, rp, v_r, LD, wmd_p, err, n,
                                           counter, s, config, dws)
     ev[2].record()
-    wmd_h = out.view(nq, N).cpu().numpy()
-    err_h = err.view(nq, _lib.ERR_WORDS).cpu().numpy()
+    # one pinned device->host copy of every query's distances and error record
+    host = ws.pinned("batch32_out", (nq * N + 1) // 2 + nq * _lib.ERR_WORDS, torch.int64)
+    h_wmd = host[: (nq * N + 1) // 2].view(torch.float32)[: nq * N]
+    h_err = host[(nq * N + 1) // 2:]
+    h_wmd.copy_(out, non_blocking=True)
+    h_err.copy_(err, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    wmd_h = h_wmd.numpy().reshape(nq, N).astype(np.float64)   # one pass: float64 results
+    err_h = h_err.numpy().reshape(nq, _lib.ERR_WORDS)
     t_dist = ev[0].elapsed_time(ev[1]) / 1e3
     t_iter = ev[1].elapsed_time(ev[2]) / 1e3
     t_total = time.perf_counter() - t_start
@@ -169,7 +221,7 @@ def solve_batch_f32(queries, corpus, embeddings, config, ws) -> list:
             continue
         timings = {"select": t_select / nq, "distances": t_dist / nq, "precompute": 0.0,
                    "init": 0.0, "iterations": t_iter / nq, "final": 0.0, "total": t_total / nq}
-        results[k] = SolverResult(wmd=wmd_h[n].astype(np.float64), iterations_run=iters[n],
+        results[k] = SolverResult(wmd=wmd_h[n], iterations_run=iters[n],
                                   converged=conv[n], timings=timings)
     return results
 

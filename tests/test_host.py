@@ -217,3 +217,17 @@ def test_embedding_fingerprint_sees_one_element_edits():
     R = E.copy()
     R.flags.writeable = False
     assert _read_only(R)
+
+
+def test_every_package_module_imports():
+    """Modules imported lazily on the GPU paths (batch, baseline, distributed)
+    must at least import on a CPU-only box."""
+    import importlib
+    import pkgutil
+
+    import paper_2107_06433_b200 as pkg
+
+    for m in pkgutil.iter_modules(pkg.__path__):
+        if m.name.startswith("lib"):          # libswmd.so: the ctypes library, not a module
+            continue
+        importlib.import_module(f"paper_2107_06433_b200.{m.name}")
