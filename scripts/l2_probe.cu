@@ -35,6 +35,59 @@ __global__ void gather_rows(const double2* __restrict__ t, int64_t n_rows, int r
     if (acc == 12345.678) *sink = acc;
 }
 
+// the c2 solve's access pattern: lane pair g of a warp gathers its own 160 B
+// row, lane h of the pair the interleaved 16-byte chunks h, h+2, ..; U rows
+// per lane pair in flight (16 U rows per warp)
+template <int U>
+__global__ void gather_pairs(const double2* __restrict__ t, int64_t n_rows, int64_t n_gathers,
+                             double* sink) {
+    const int lane = threadIdx.x & 31, g = lane >> 1, h = lane & 1;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double acc = 0;
+    uint32_t x = 2463534242u ^ (uint32_t)(warp * 32 + g);
+    for (int64_t base = warp * 16 * U; base < n_gathers; base += nwarps * 16 * U) {
+        double2 v[U][5];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+            const double2* row = t + (int64_t)(x % n_rows) * 10 + h;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) v[u][k] = __ldg(row + 2 * k);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc += v[u][k].x + v[u][k].y;
+    }
+    if (acc == 12345.678) *sink = acc;
+}
+
+// best-case 160 B row gather: 10 consecutive lanes read one row's ten 16-byte
+// chunks in one instruction (5 full sectors), 3 rows per warp-instruction,
+// U instructions in flight
+template <int U>
+__global__ void gather_rows10(const double2* __restrict__ t, int64_t n_rows, int64_t n_gathers,
+                              double* sink) {
+    const int lane = threadIdx.x & 31, grp = lane / 10, c = lane % 10;
+    const bool on = lane < 30;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double acc = 0;
+    uint32_t x = 2463534242u ^ (uint32_t)(warp * 4 + grp);
+    for (int64_t base = warp * 3 * U; base < n_gathers; base += nwarps * 3 * U) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+            v[u] = on ? __ldg(t + (int64_t)(x % n_rows) * 10 + c) : make_double2(0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y;
+    }
+    if (acc == 12345.678) *sink = acc;
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -83,6 +136,52 @@ int main() {
                    (double)ng * row_bytes / (ms * 1e-3) / 1e12);
             cudaFree(t);
         }
+    }
+    // the c2 K-row pattern: 160 B rows, lane pairs, 16 x U rows per warp in flight
+    for (int64_t mb : {16, 64}) {
+        const int64_t bytes = mb << 20;
+        double2* t;
+        cudaMalloc(&t, bytes);
+        cudaMemset(t, 0, bytes);
+        const int64_t n_rows = bytes / 160;
+        const int64_t ng = (int64_t)16 << 20;
+        for (int wps : {16, 32, 64}) {
+            for (int U : {1, 2, 4}) {
+                auto run = [&](int64_t n) {
+                    if (U == 1) gather_pairs<1><<<sms * wps / 8, 256>>>(t, n_rows, n, sink);
+                    else if (U == 2) gather_pairs<2><<<sms * wps / 8, 256>>>(t, n_rows, n, sink);
+                    else gather_pairs<4><<<sms * wps / 8, 256>>>(t, n_rows, n, sink);
+                };
+                run(ng / 4);
+                cudaEventRecord(a);
+                run(ng);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                printf("pairs   row  160 B  table %3lld MB  warps/SM %2d  rows/pair %d: %.1f TB/s\n",
+                       (long long)mb, wps, U, (double)ng * 160 / (ms * 1e-3) / 1e12);
+            }
+        }
+        for (int wps : {16, 32, 64}) {
+            for (int U : {2, 4, 8}) {
+                auto run = [&](int64_t n) {
+                    if (U == 2) gather_rows10<2><<<sms * wps / 8, 256>>>(t, n_rows, n, sink);
+                    else if (U == 4) gather_rows10<4><<<sms * wps / 8, 256>>>(t, n_rows, n, sink);
+                    else gather_rows10<8><<<sms * wps / 8, 256>>>(t, n_rows, n, sink);
+                };
+                run(ng / 4);
+                cudaEventRecord(a);
+                run(ng);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                printf("rows10  row  160 B  table %3lld MB  warps/SM %2d  in flight %d: %.1f TB/s\n",
+                       (long long)mb, wps, U, (double)ng * 160 / (ms * 1e-3) / 1e12);
+            }
+        }
+        cudaFree(t);
     }
     return 0;
 }
