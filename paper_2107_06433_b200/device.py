@@ -59,7 +59,14 @@ def device(index: int | None = None) -> torch.device:
     return d
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_ptr(dev: torch.device | None = None) -> int:
+    """cudaStream_t of the current stream on ``dev`` (the per-query path calls
+    this every time: the raw accessor skips torch's Stream object)."""
+    if _RAW_STREAM is not None and dev is not None and dev.index is not None:
+        return int(_RAW_STREAM(dev.index))
     return torch.cuda.current_stream(dev).cuda_stream
 
 

@@ -658,9 +658,9 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
             raise _lib.NativeError(f"swmd_plan_run: CUDA error {rc}")
         if rc == 0 and plan.err[0] == _lib.NO_EVENT and plan.err[1] == _lib.NO_EVENT:
             t = plan.times
-            timings = phase_timings(
-                {"select": float(t[2]) / 1e3, "total": time.perf_counter() - t_start},
-                {"distances": float(t[0]) / 1e3, "iterations": float(t[1]) / 1e3})
+            timings = {"select": float(t[2]) / 1e3, "distances": float(t[0]) / 1e3,
+                       "precompute": 0.0, "init": 0.0, "iterations": float(t[1]) / 1e3,
+                       "final": 0.0, "total": time.perf_counter() - t_start}   # PHASES order
             return SolverResult(wmd=wmd, iterations_run=config.max_iter, converged=False,
                                 timings=timings)
         # rc == -4 (outside the native fast path) or a degeneracy to decode:

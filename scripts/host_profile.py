@@ -12,6 +12,7 @@ import paper_2107_06433_b200 as swmd
 from paper_2107_06433_b200 import synth
 
 inst = synth.zipf_instance("c2")
+inst.embeddings.flags.writeable = False   # a serving table: resident copy keyed by identity
 corpus = inst.corpus()
 cfg = swmd.SolverConfig()
 ws = swmd.SinkhornWorkspace()
