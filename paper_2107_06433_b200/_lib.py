@@ -102,7 +102,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         )
     lib = ctypes.CDLL(path)
     for name, argtypes in _SIGS.items():
-        fn = getattr(lib, name)
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            if os.path.abspath(path) != os.path.abspath(LIB_PATH):
+                continue      # an older experiment build (SWMD_LIB): only what it has
+            raise
         fn.argtypes = argtypes
         fn.restype = _RESTYPE.get(name, ctypes.c_int)
     return lib
