@@ -273,6 +273,10 @@ int swmd_update_u_f64(const double* x, double* u, int64_t n, int32_t code,
  * entry (EmptyQueryError). */
 int64_t swmd_select_query(const double* r, int64_t n, int64_t* stage, int64_t cap);
 
+/* HOST function: memcpy of `bytes` from src to dst split over `threads`
+ * threads (result buffers of a batch, detached from the pinned workspace). */
+int swmd_host_copy(void* dst, const void* src, int64_t bytes, int32_t threads);
+
 /*
  * Native per-query runtime (replaces the Python orchestration of
  * solver.py:106-201 for the common case tol == NULL, v_r <= 32).

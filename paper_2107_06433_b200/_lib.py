@@ -67,6 +67,7 @@ _SIGS = {
                                _I64, _P, _P],
     "swmd_l2_flush": [_P, _I64, _P],
     "swmd_select_query": [_P, _I64, _P, _I64],
+    "swmd_host_copy": [_P, _P, _I64, _I32],
     "swmd_row_norms_f32": [_P, _I64, _I32, _I64, _P, _P],
     "swmd_cost_build_batch_f32": [_P, _I64, _I32, _I64, _P, _P, _I32, ctypes.c_float, _P, _P,
                                   _I64, _P, _P, _P],

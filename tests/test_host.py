@@ -231,3 +231,30 @@ def test_every_package_module_imports():
         if m.name.startswith("lib"):          # libswmd.so: the ctypes library, not a module
             continue
         importlib.import_module(f"paper_2107_06433_b200.{m.name}")
+
+
+def test_native_select_matches_select_nonzero():
+    """swmd_select_query (the native scan behind the public API and the batch
+    path) returns select_nonzero's (sel, weights) and raises its errors
+    (kernels.py:74-88), NaN entries skipped like numpy's r > 0."""
+    import numpy as np
+
+    from paper_2107_06433_b200.kernels import EmptyQueryError, select_nonzero
+    from paper_2107_06433_b200.solver import SinkhornWorkspace, select_native
+
+    rng = np.random.default_rng(3)
+    ws = SinkhornWorkspace()
+    for n in (1, 31, 32, 33, 100, 5000):
+        for _ in range(10):
+            q = np.zeros(n)
+            k = int(rng.integers(1, min(n, 300) + 1))
+            idx = rng.choice(n, size=k, replace=False)
+            q[idx] = rng.random(k) + 1e-3
+            if n > 40:
+                q[rng.choice(n, 3, replace=False)] = np.nan
+            a, b = select_native(q, ws), select_nonzero(q)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    with pytest.raises(ValueError, match="nonnegative"):
+        select_native(np.array([0.0, -1.0, 2.0]), ws)
+    with pytest.raises(EmptyQueryError):
+        select_native(np.zeros(64), ws)
