@@ -306,6 +306,16 @@ int swmd_plan_run(swmd_plan* plan, const double* query, int64_t V, double lam,
                   int32_t max_iter, int32_t cost_mode, double* wmd_host,
                   int64_t* err_host, float* times_ms, int64_t* v_r_out);
 
+/* swmd_plan_run with the distances (n_cols doubles) and the 4-word error
+ * record written to caller device buffers and nothing copied back: the
+ * work is only enqueued on the plan's stream (no synchronisation), so the
+ * caller's next stream operation — the multi-GPU path's all-gather of the
+ * distance slots (distributed.py) — consumes them in place.  Same return
+ * codes as swmd_plan_run (-4: outside the native fast path). */
+int swmd_plan_run_device(swmd_plan* p, const double* query, int64_t V, double lam,
+                         int32_t max_iter, int32_t cost_mode, double* wmd_dev,
+                         int64_t* err_dev, int64_t* v_r_out);
+
 /*
  * Device CSR -> CSC transpose (replaces the host argsort of
  * CsrMatrix.csc_index, sparse.py:98-120): from row_ptr (n_rows+1), col_idx,

@@ -91,16 +91,51 @@ class DeviceShardSolver:
         return solve_on_device(sel, weights, self.block(c0, c1), self.de, config, self.ws,
                                allreduce_max=allreduce_max)
 
-    def solve_into(self, sel, weights, c0, c1, config, allreduce_max, slot: torch.Tensor):
+    def solve_into(self, sel, weights, c0, c1, config, allreduce_max, slot: torch.Tensor,
+                   query: np.ndarray | None = None):
         """Solve the block with ``slot[:c1-c0]`` (float64, on this device) as
         the distance buffer and the error record written to
         ``slot[width:width+4]`` (int64 bits).  Returns (iterations,
-        converged, decode) — ``decode(err_words)`` yields the block's DegEvent."""
-        from .solver import QueryPlan, _device_spans, _Events
+        converged, decode, spans) — ``decode(err_words)`` yields the block's
+        DegEvent, ``spans(gathered_slot)`` the device phase times.
+
+        tol unset and a dense float64 query: the native per-query runtime
+        (one C call: select, one CUDA-graph launch, results left in the slot,
+        phase stamps copied next to them) — nothing is synchronised before the
+        caller's all-gather."""
+        from .solver import QueryPlan, _device_spans, _Events, _native_plan
 
         dc = self.block(c0, c1)
-        plan = QueryPlan(sel, weights, dc, self.de, config, self.ws)
         width = slot.numel() - _TAIL
+        if (config.tol is None and query is not None and query.dtype == np.float64
+                and query.ndim == 1 and query.flags.c_contiguous and dc.n_cols > 0):
+            nplan = _native_plan(self.ws, dc, self.de, dc.device)
+            err_view = slot[width: width + 4].view(torch.int64)
+            rc = nplan.run_device(query, config, slot.data_ptr(), err_view.data_ptr())
+            if rc == 0:
+                n = dc.n_cols
+                slot[width + 6: width + 9].view(torch.int64).copy_(
+                    nplan.out_dev[n + 4: n + 7])
+
+                def decode(_words):      # rare error path: replay to name the event exactly
+                    qp = QueryPlan(sel, weights, dc, self.de, config, self.ws)
+                    qp.enqueue_distances()
+                    qp.enqueue_solve()
+                    return qp.decode_event(qp.readback()[1])
+
+                def spans(row):
+                    st = np.asarray(row[width + 6: width + 9]).view(np.int64)
+                    return {"distances": (st[1] - st[0]) * 1e-9, "precompute": 0.0,
+                            "init": 0.0, "iterations": (st[2] - st[1]) * 1e-9, "final": 0.0}
+
+                return config.max_iter, False, decode, spans
+            if rc > 0:
+                from . import _lib
+
+                raise _lib.NativeError(f"swmd_plan_run_device: CUDA error {rc}")
+            # rc < 0: outside the native fast path (argument errors were raised by
+            # select_nonzero already): the general path below
+        plan = QueryPlan(sel, weights, dc, self.de, config, self.ws)
         plan.wmd = slot[: c1 - c0]
         plan.err = slot[width: width + 4].view(torch.int64)
         ev = _Events(True)
@@ -113,12 +148,13 @@ class DeviceShardSolver:
         else:
             iterations, converged = plan.run_tol(allreduce_max)
         ev.mark("i1")
-        return iterations, converged, plan.decode_event, lambda: _device_spans(ev)
+        return iterations, converged, plan.decode_event, lambda _row: _device_spans(ev)
 
 
 # per-rank gather slot: distances (padded to the widest block) | the block's
-# error record (4 int64 words, swmd.h) | iterations run | converged
-_TAIL = 6
+# error record (4 int64 words, swmd.h) | iterations run | converged | the
+# native runtime's 3 device clock stamps (int64 bits; zero on other paths)
+_TAIL = 9
 
 
 def merge_events(events: list[DegEvent | None]) -> DegEvent | None:
@@ -172,7 +208,7 @@ def sinkhorn_wmd_sharded(query, corpus, embeddings, config: SolverConfig,
     slot = torch.zeros(width + _TAIL, dtype=torch.float64, device=cdev)
     if isinstance(solver, DeviceShardSolver) and cdev.type == "cuda":
         iterations, converged, decode, spans = solver.solve_into(sel, weights, c0, c1, config,
-                                                                 arm, slot)
+                                                                 arm, slot, query=query)
     else:
         res = solver(sel, weights, c0, c1, config, arm)
         host = np.zeros(width + _TAIL, dtype=np.float64)
@@ -183,7 +219,7 @@ def sinkhorn_wmd_sharded(query, corpus, embeddings, config: SolverConfig,
             words[0] = 0                      # "this block has an event"
         iterations, converged = res.iterations, res.converged
         decode = lambda _words, ev=res.event: ev   # noqa: E731
-        spans = lambda t=res.timings: t   # noqa: E731
+        spans = lambda _row, t=res.timings: t   # noqa: E731
         slot.copy_(torch.from_numpy(host))
     slot[width + 4] = float(iterations)
     slot[width + 5] = 1.0 if converged else 0.0
@@ -218,7 +254,7 @@ def sinkhorn_wmd_sharded(query, corpus, embeddings, config: SolverConfig,
         a, b = int(bounds[r]), int(bounds[r + 1])
         wmd[a:b] = allv[r, : b - a]
     timings = phase_timings({"select": t_select, "total": time.perf_counter() - t_start},
-                            spans())
+                            spans(allv[rank]))
     return SolverResult(wmd=wmd, iterations_run=int(allv[0, width + 4]),
                         converged=bool(allv[0, width + 5]), timings=timings)
 

@@ -602,6 +602,14 @@ class NativePlan:
         except Exception:
             pass
 
+    def run_device(self, q: np.ndarray, config: SolverConfig, wmd_ptr: int, err_ptr: int) -> int:
+        """Enqueue the query with results left in device buffers (no sync).
+        Returns rc: 0 ok, -2/-3 argument errors, -4 general path."""
+        mode = COST_MODE_GRAM if config.cost_mode == "gram" else COST_MODE_DIRECT
+        return _lib.lib().swmd_plan_run_device(self.handle, q.ctypes.data, q.size,
+                                               float(config.lam), int(config.max_iter), mode,
+                                               wmd_ptr, err_ptr, self.vr.ctypes.data)
+
     def run(self, q: np.ndarray, config: SolverConfig):
         """Returns (rc, wmd).  rc: 0 ok, -2/-3 argument errors, -4 general path."""
         wmd = np.empty(self.dc.n_cols, dtype=np.float64)
