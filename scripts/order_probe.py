@@ -65,6 +65,8 @@ rounds = (lens + 15) // 16
 slab = (np.clip(lens - 32, 0, 48) + 15) // 16
 for label, (f, r, sl) in {"r1 model 0.55/0.14/0.33": (0.55, 0.14, 0.33),
                           "flat 0.3/0.3/0.3": (0.3, 0.3, 0.3),
+                          "r2 trace fit 0.5/0.02/0.2": (0.5, 0.02, 0.2),
+                          "r2 trace fit x 0.5/0.1/0.25": (0.5, 0.1, 0.25),
                           "fixed-heavy 0.8/0.1/0.3": (0.8, 0.1, 0.3),
                           "slab-heavy 0.4/0.2/0.5": (0.4, 0.2, 0.5)}.items():
     cost = f + r * np.minimum(rounds, 2) + sl * slab
