@@ -147,3 +147,21 @@ def test_check_topk_rules():
         check_topk(bad, idx, ref[idx], 3, ref_full=ref)
     with pytest.raises(AssertionError):                 # outside doc, no boundary tie
         check_topk(bad, idx[:4], ref[idx][:4], 3)
+
+
+def test_oracle_pinned_on_edge_cases(oracle_lib):
+    """The oracle against the reference's edge-case runs (tests/golden/edge.npz):
+    max_iter = 1, float32 embeddings coerced to float64, tol = 0."""
+    from paper_2107_06433_b200.sparse import CsrMatrix
+
+    g = golden("edge")
+    V, N = g["emb"].shape[0], g["wmd_iter1"].shape[0]
+    cp, rows, _, vals = CsrMatrix(V, N, g["row_ptr"], g["col_idx"], g["values"]).csc_index()
+    r = oracle_lib.solve(g["q"], cp, rows, vals, g["emb"], lam=10.0, max_iter=1)
+    assert np.array_equal(r.wmd, g["wmd_iter1"])
+    r = oracle_lib.solve(g["q"], cp, rows, vals, g["emb"].astype(np.float32).astype(np.float64),
+                         lam=10.0, max_iter=15)
+    assert np.array_equal(r.wmd, g["wmd_f32emb"])
+    r = oracle_lib.solve(g["q"], cp, rows, vals, g["emb"], lam=10.0, max_iter=9, tol=0.0)
+    assert np.array_equal(r.wmd, g["wmd_tol0"])
+    assert r.iterations_run == int(g["tol0_iters"]) and r.converged == bool(g["tol0_conv"])
