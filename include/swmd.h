@@ -306,6 +306,14 @@ int swmd_plan_run(swmd_plan* plan, const double* query, int64_t V, double lam,
                   int32_t max_iter, int32_t cost_mode, double* wmd_host,
                   int64_t* err_host, float* times_ms, int64_t* v_r_out);
 
+/* swmd_plan_run for a query already in selected form (ascending unique word
+ * ids sel[0:v_r] and positive weights — a SparseVector histogram, the
+ * reference's ingest output): no dense scan.  -4 when the selection is not
+ * valid or too wide for the native path (the caller's general path decides). */
+int swmd_plan_run_selected(swmd_plan* p, const int64_t* sel, const double* weights,
+                           int64_t v_r, double lam, int32_t max_iter, int32_t cost_mode,
+                           double* wmd_host, int64_t* err_host, float* times_ms);
+
 /* swmd_plan_run with the distances (n_cols doubles) and the 4-word error
  * record written to caller device buffers and nothing copied back: the
  * work is only enqueued on the plan's stream (no synchronisation), so the

@@ -85,6 +85,7 @@ _SIGS = {
     "swmd_plan_destroy": [_P],
     "swmd_plan_run": [_P, _P, _I64, _D, _I32, _I32, _P, _P, _P, _P],
     "swmd_plan_run_device": [_P, _P, _I64, _D, _I32, _I32, _P, _P, _P],
+    "swmd_plan_run_selected": [_P, _P, _P, _I64, _D, _I32, _I32, _P, _P, _P],
     "swmd_schedule_order": [_P, _I64, _I32, _I32, _I32, _I32, _P],
     "swmd_solve_slots_f64": [_I32, _P],
     "swmd_solve_reg_rounds_f64": [_I32],

@@ -504,6 +504,13 @@ def solve_on_device(sel: np.ndarray | None, weights: np.ndarray | None, dc: Devi
     return ShardResult(wmd_host, iterations, converged, _device_spans(ev), event)
 
 
+def _is_sparse_vector(q) -> bool:
+    """This package's SparseVector or the reference's (same attributes)."""
+    return isinstance(q, SparseVector) or (
+        not isinstance(q, np.ndarray) and hasattr(q, "indices") and hasattr(q, "values")
+        and hasattr(q, "length") and hasattr(q, "to_dense"))
+
+
 def select_native(query: np.ndarray, ws: SinkhornWorkspace) -> tuple[np.ndarray, np.ndarray]:
     """``select_nonzero`` (kernels.py:74-88) through the native scan
     (swmd_select_query): the same ``(sel, weights)``, errors and messages, at
@@ -610,6 +617,17 @@ class NativePlan:
                                                float(config.lam), int(config.max_iter), mode,
                                                wmd_ptr, err_ptr, self.vr.ctypes.data)
 
+    def run_selected(self, indices: np.ndarray, values: np.ndarray, config: SolverConfig):
+        """``run`` for an already-selected query (SparseVector): (rc, wmd)."""
+        sel = np.ascontiguousarray(indices, dtype=np.int64)
+        w = np.ascontiguousarray(values, dtype=np.float64)
+        wmd = np.empty(self.dc.n_cols, dtype=np.float64)
+        mode = COST_MODE_GRAM if config.cost_mode == "gram" else COST_MODE_DIRECT
+        rc = _lib.lib().swmd_plan_run_selected(self.handle, sel.ctypes.data, w.ctypes.data,
+                                               sel.size, float(config.lam), int(config.max_iter),
+                                               mode, wmd.ctypes.data, self._args[0], self._args[1])
+        return rc, wmd
+
     def run(self, q: np.ndarray, config: SolverConfig):
         """Returns (rc, wmd).  rc: 0 ok, -2/-3 argument errors, -4 general path."""
         wmd = np.empty(self.dc.n_cols, dtype=np.float64)
@@ -636,16 +654,36 @@ def sinkhorn_wmd(query, corpus, embeddings, config: SolverConfig,
     """Regularised transport distance of one query to every corpus column
     (solver.py:106-201), on the current CUDA device."""
     t_start = time.perf_counter()
-    if isinstance(query, SparseVector):
-        query = query.to_dense()
-    query = np.asarray(query, dtype=np.float64)
     n_vocab = corpus.n_rows
     emb_shape = tuple(embeddings.shape)
+    ws = workspace if workspace is not None else _default_ws()
+    if _is_sparse_vector(query):
+        # the reference's ingest hands queries over as SparseVector histograms
+        # (ingest.py:175-197): already selected, so the native runtime takes
+        # (ids, weights) directly — no densify, no scan of V entries
+        if (config.tol is None and config.precision == "f64" and config.workers <= 1
+                and int(query.length) == n_vocab and emb_shape[0] == n_vocab
+                and corpus.n_cols > 0 and 0 < query.indices.size <= 32 and cuda_ok()):
+            dev = device()
+            dc = DeviceCorpus.of(corpus, dev)
+            de = DeviceEmbeddings.of(embeddings, dev)
+            plan = _native_plan(ws, dc, de, dev)
+            rc, wmd = plan.run_selected(query.indices, query.values, config)
+            if rc > 0:
+                raise _lib.NativeError(f"swmd_plan_run_selected: CUDA error {rc}")
+            if rc == 0 and plan.err[0] == _lib.NO_EVENT and plan.err[1] == _lib.NO_EVENT:
+                t = plan.times
+                timings = {"select": float(t[2]) / 1e3, "distances": float(t[0]) / 1e3,
+                           "precompute": 0.0, "init": 0.0, "iterations": float(t[1]) / 1e3,
+                           "final": 0.0, "total": time.perf_counter() - t_start}
+                return SolverResult(wmd=wmd, iterations_run=config.max_iter, converged=False,
+                                    timings=timings)
+        query = query.to_dense()
+    query = np.asarray(query, dtype=np.float64)
     if query.shape != (n_vocab,) or emb_shape[0] != n_vocab:
         raise ValueError(
             f"shape mismatch: query {query.shape}, embeddings "
             f"{emb_shape}, corpus rows {n_vocab}")
-    ws = workspace if workspace is not None else _default_ws()
     if config.workers > 1 and config.precision == "f64" and corpus.n_cols > 1 and cuda_ok():
         n_dev = min(config.workers, torch.cuda.device_count())
         if n_dev > 1:   # workers -> GPUs (SURVEY §8(b)3): one column block per device

@@ -69,3 +69,23 @@ def test_empty_corpus(edge):
     assert r.iterations_run == int(g["empty_iters"]) and r.converged == bool(g["empty_conv"])
     unf = swmd.unfused_sparse_wmd(g["q"], empty, g["emb"], swmd.SolverConfig(max_iter=3))
     assert unf.shape == (0,)
+
+
+def test_sparse_vector_query_native_path_same_bits():
+    """A SparseVector query (the reference's ingest output) goes through the
+    native runtime without densifying; the distances are the dense query's."""
+    from paper_2107_06433_b200 import synth
+    from paper_2107_06433_b200.sparse import SparseVector
+
+    inst = synth.zipf_instance("c2")
+    corpus = inst.corpus()
+    sel = np.flatnonzero(inst.query > 0)
+    sv = SparseVector(inst.query.size, sel, inst.query[sel])
+    cfg = swmd.SolverConfig(lam=10.0, max_iter=15)
+    dense = swmd.sinkhorn_wmd(inst.query, corpus, inst.embeddings, cfg)
+    sparse = swmd.sinkhorn_wmd(sv, corpus, inst.embeddings, cfg)
+    assert np.array_equal(dense.wmd, sparse.wmd)
+    assert max_rel_err(sparse.wmd, golden("c2")["wmd"]) <= RTOL
+    # an empty histogram still raises the reference's error
+    with pytest.raises(swmd.EmptyQueryError):
+        swmd.sinkhorn_wmd(SparseVector(inst.query.size, [], []), corpus, inst.embeddings, cfg)
