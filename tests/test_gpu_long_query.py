@@ -1,0 +1,113 @@
+"""The long-query solve (32 < v_r <= 256, `cta2_solve`: a CTA per column, two
+K rows reduced per warp step) against the CPU oracle: every row-width
+instantiation (1-4 sixteen-byte chunks per lane, rows that fill their last
+chunk and rows that do not), columns shorter than one CTA step and longer
+than the staged index arrays, the reference's degeneracy messages, the tol
+path and the shard split.  Reference: _jit.py:164-183, 291-312 at large v_r.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import max_rel_err
+
+import paper_2107_06433_b200 as swmd
+from paper_2107_06433_b200 import synth
+from paper_2107_06433_b200.sparse import CsrMatrix
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    swmd.kernels.warmup()
+
+
+def _case(seed, V, N, kmin, kmax, v_r, dim=48):
+    rng = np.random.default_rng(seed)
+    emb = synth.normal_embeddings(rng, V, dim)
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, kmin, kmax)
+    q = synth.zipf_query(rng, V, v_r)
+    return q, CsrMatrix.from_csc(V, N, cp, rows, vals), emb, (cp, rows, vals)
+
+
+# ldk = v_r rounded up to 4; chunks per lane = ceil(ldk / 64); "whole" rows: ldk == 64 * chunks
+@pytest.mark.parametrize("v_r", [33, 40, 61, 64, 65, 96, 127, 128, 129, 150, 190, 192, 193,
+                                 200, 250, 253, 256])
+def test_row_width_instantiations(v_r, oracle_lib):
+    q, corpus, emb, (cp, rows, vals) = _case(500 + v_r, 3000, 140, 1, 70, v_r)
+    got = swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig(lam=10.0, max_iter=15)).wmd
+    want = oracle_lib.solve(q, cp, rows, vals, emb, lam=10.0, max_iter=15).wmd
+    assert max_rel_err(got, want) <= RTOL
+
+
+@pytest.mark.parametrize("v_r", [70, 256])
+def test_columns_longer_than_the_staged_index(v_r, oracle_lib):
+    """Columns of 450-700 nonzeros: some fit the 512-entry staged (row id,
+    value) arrays, some are read from global memory."""
+    q, corpus, emb, (cp, rows, vals) = _case(77 + v_r, 4000, 20, 450, 700, v_r, dim=32)
+    assert int(np.diff(cp).max()) > 512 and int(np.diff(cp).min()) < 512
+    got = swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig(lam=5.0, max_iter=6)).wmd
+    want = oracle_lib.solve(q, cp, rows, vals, emb, lam=5.0, max_iter=6).wmd
+    assert max_rel_err(got, want) <= RTOL
+
+
+@pytest.mark.parametrize("v_r", [40, 130])
+def test_zero_denominator_message_matches_oracle(v_r, oracle_lib):
+    """exp(-lam*M) underflows for far words: the first (i, j) the reference's
+    CSR walk reports, from whichever half-warp saw it."""
+    rng = np.random.default_rng(9 + v_r)
+    V, N = 400, 30
+    emb = rng.normal(size=(V, 4)) * 30
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, 2, 40)
+    corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+    q = np.zeros(V)
+    q[rng.choice(V, size=v_r, replace=False)] = 1.0 / v_r
+    cfg = swmd.SolverConfig(lam=50.0, max_iter=4)
+    with pytest.raises(swmd.DegeneracyError) as exc:
+        swmd.sinkhorn_wmd(q, corpus, emb, cfg)
+    with pytest.raises(oracle_lib.OracleDegeneracy) as want:
+        oracle_lib.solve(q, cp, rows, vals, emb, lam=50.0, max_iter=4)
+    assert str(exc.value) == str(want.value)
+
+
+def test_tol_path_matches_oracle(oracle_lib):
+    """One launch per iteration with x carried through HBM (x_in / x_out)."""
+    q, corpus, emb, (cp, rows, vals) = _case(4242, 2500, 90, 3, 60, 80)
+    cfg = swmd.SolverConfig(lam=1.0, max_iter=60, tol=1e-9)
+    res = swmd.sinkhorn_wmd(q, corpus, emb, cfg)
+    want = oracle_lib.solve(q, cp, rows, vals, emb, lam=1.0, max_iter=60, tol=1e-9)
+    assert res.iterations_run == want.iterations_run and res.converged == want.converged
+    assert max_rel_err(res.wmd, want.wmd) <= RTOL
+
+
+def test_max_iter_one_and_empty_column_free_corpus(oracle_lib):
+    q, corpus, emb, (cp, rows, vals) = _case(31337, 2000, 64, 1, 9, 200)
+    got = swmd.sinkhorn_wmd(q, corpus, emb, swmd.SolverConfig(lam=10.0, max_iter=1)).wmd
+    want = oracle_lib.solve(q, cp, rows, vals, emb, lam=10.0, max_iter=1).wmd
+    assert max_rel_err(got, want) <= RTOL
+
+
+def test_column_blocks_are_bitwise_identical():
+    """Each column is solved by one CTA whatever the block it arrives in, so
+    the shard split cannot change a bit (distributed.py, sparse.py:261-276)."""
+    from paper_2107_06433_b200.distributed import DeviceShardSolver, shard_bounds
+
+    q, corpus, emb, _ = _case(2024, 3000, 200, 5, 90, 256)
+    cfg = swmd.SolverConfig(lam=10.0, max_iter=15)
+    one = swmd.sinkhorn_wmd(q, corpus, emb, cfg).wmd
+    sel, w = swmd.select_nonzero(q)
+    solver = DeviceShardSolver(corpus, emb)
+    for world in (2, 3):
+        b = shard_bounds(corpus, world)
+        got = np.concatenate([solver(sel, w, int(b[r]), int(b[r + 1]), cfg, None).wmd
+                              for r in range(world)])
+        assert np.array_equal(got, one), world
