@@ -649,15 +649,19 @@ def run_b200(args):
     flops = iters * (4 * nnz_loc * v_r + 2 * nnz_loc + dc.n_cols * v_r) + 6 * nnz_loc * v_r
     dominant = "solve" if s_ms >= c_ms else "cost"
     ncu = {}
-    ncu_src = "profiles/r02_ncu_c2.json"
+    # the committed --set full capture of this config's dominant kernel, if there is one
+    ncu_src = f"profiles/r02_ncu_{args.config}.json"
     try:
         with open(os.path.join(REPO, ncu_src)) as f:
             ncu = json.load(f)["kernels"]
     except (OSError, KeyError, ValueError):
         pass
-    kname = "reg_solve" if dominant == "solve" else "cost_tmap_kernel"
+    if dominant != "solve":
+        kname = "cost_tmap_kernel"
+    else:
+        kname = "reg_solve" if v_r <= 32 else "cta2_solve"
     traffic = None
-    if kname in ncu and args.config == "c2" and world == 1:
+    if kname in ncu and args.config in ("c2", "c3", "c5") and world == 1:
         traffic = ncu[kname]["dram_read_bytes"] + ncu[kname]["dram_write_bytes"]
     if dominant == "solve":
         achieved = solve_bytes / (s_ms / 1e3) / 1e9

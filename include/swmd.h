@@ -153,6 +153,27 @@ int swmd_solve_f64_reset_done(const int64_t* col_ptr, const int32_t* rows, const
                               const double* x_in, double* x_out, double* wmd,
                               int64_t col_key_offset, int64_t n_key, int32_t group_hint,
                               int32_t max_len_hint, int64_t* err, int32_t* counter, void* stream);
+/* swmd_solve_f64 for long queries (32 < v_r <= 256, the per-column gather of
+ * _jit.py:164-183 / 291-312 at large v_r, where K no longer fits L2) with the
+ * corpus's hot-row index: hot_slot[i] is the rank of vocabulary row i among
+ * the corpus's n_hot most frequent rows (-1 when it is not one of them) and
+ * hot_ids[s] the row of rank s.  The launch keeps the K rows of as many of
+ * those ranks as fit beside its working set in shared memory (one CTA per SM,
+ * several columns in flight per CTA sharing the slab), so the Zipf head of
+ * the vocabulary is read from L2 once per launch instead of once per nonzero
+ * and pass.  Results are bitwise those of swmd_solve_f64 (same rows, same
+ * order; only where a row is read from differs).  Both index pointers NULL or
+ * n_hot = 0: identical to swmd_solve_f64 / _reset_done (counter_zeroed != 0). */
+int swmd_solve_hot_f64(const int64_t* col_ptr, const int32_t* rows, const double* vals,
+                       int64_t n_cols, const int32_t* order,
+                       const double* kernel, const double* kernel_cost,
+                       const double* weights, int32_t v_r, int64_t ldk,
+                       int32_t t_begin, int32_t t_end,
+                       const double* x_in, double* x_out, double* wmd,
+                       int64_t col_key_offset, int64_t n_key, int32_t group_hint,
+                       int32_t max_len_hint, int64_t* err, int32_t* counter, void* stream,
+                       int32_t counter_zeroed, const int32_t* hot_slot, const int32_t* hot_ids,
+                       int32_t n_hot);
 
 /*
  * fp32 multi-query variant (BASELINE config c4; the reference is fp64-only,

@@ -55,6 +55,8 @@ _SIGS = {
                        _I64, _I64, _I32, _I32, _P, _P, _P],
     "swmd_solve_f64_reset_done": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P,
                                   _P, _P, _I64, _I64, _I32, _I32, _P, _P, _P],
+    "swmd_solve_hot_f64": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _P, _P, _P,
+                           _I64, _I64, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I32],
     "swmd_fused_iteration_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _P],
     "swmd_fused_final_f64": [_P, _P, _P, _I64, _P, _P, _I32, _I64, _P, _P, _I64, _P, _P],
     "swmd_sddmm_f64": [_P, _P, _P, _P, _I64, _P, _I32, _I64, _P, _P, _I64, _P, _P],

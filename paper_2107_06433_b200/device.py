@@ -140,6 +140,30 @@ class DeviceCorpus:
         self._pos_host = pos
         self._pos = None
 
+    HOT_ROWS = 256   # ranks kept in the hot-row index (a launch uses as many as fit its slab)
+
+    def hot_index(self):
+        """(hot_slot, hot_ids) of swmd_solve_hot_f64, built on the device at the
+        first long-query solve: the corpus's most frequent vocabulary rows by
+        nonzero count (ties to the lower row id), or (None, None) for an empty
+        corpus."""
+        hot = getattr(self, "_hot", None)
+        if hot is None:
+            if self.nnz == 0 or self.n_rows == 0:
+                hot = (None, None)
+            else:
+                counts = torch.bincount(self.rows.to(torch.int64), minlength=self.n_rows)
+                k = int(min(self.HOT_ROWS, self.n_rows))
+                # stable: sort by (-count, row id)
+                order = torch.argsort(counts, descending=True, stable=True)[:k]
+                order = order[counts[order] > 0]
+                ids = order.to(torch.int32).contiguous()
+                slot = torch.full((self.n_rows,), -1, dtype=torch.int32, device=self.device)
+                slot[order] = torch.arange(order.numel(), dtype=torch.int32, device=self.device)
+                hot = (slot, ids) if ids.numel() else (None, None)
+            self._hot = hot
+        return hot
+
     def _set_layout(self, cp: np.ndarray, present: np.ndarray):
         lens = np.diff(cp)
         self.host_col_ptr = cp

@@ -23,6 +23,7 @@ Per-phase times come from CUDA events on the solver's stream.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -159,6 +160,12 @@ class SinkhornWorkspace:
             arr = self._pinned[name].numpy()
             cache[name] = arr
         return arr
+
+
+try:
+    _HOT_ROWS = max(0, int(os.environ.get("SWMD_CTA_HOT", "0") or 0))
+except ValueError:
+    _HOT_ROWS = 0
 
 
 def init_x(v_r: int, n_docs: int) -> np.ndarray:
@@ -378,6 +385,23 @@ class QueryPlan:
 
     def _solve(self, t0: int, t1: int, x_in, x_out, wmd, reset_done: bool = False) -> None:
         dc = self.dc
+        if 32 < self.v_r <= 256 and _HOT_ROWS > 0:
+            # long queries, opt-in (SWMD_CTA_HOT=<rows>): the corpus's hot-row
+            # index rides along (swmd.h: swmd_solve_hot_f64)
+            slot, ids = dc.hot_index()
+            _lib.call("swmd_solve_hot_f64", dc.col_ptr.data_ptr(), dc.rows.data_ptr(),
+                      dc.vals.data_ptr(), dc.n_cols, dc.order.data_ptr(), self.K.data_ptr(),
+                      self.KM.data_ptr(), self.r_dev.data_ptr(), self.v_r, self.ldk, t0, t1,
+                      x_in.data_ptr() if x_in is not None else None,
+                      x_out.data_ptr() if x_out is not None else None,
+                      wmd.data_ptr() if wmd is not None else None, dc.col_offset, dc.n_key,
+                      self.group, dc.max_len, self.err.data_ptr(), self.counter.data_ptr(),
+                      self.stream, 1 if reset_done else 0,
+                      slot.data_ptr() if slot is not None else None,
+                      ids.data_ptr() if ids is not None else None,
+                      int(ids.numel()) if ids is not None else 0)
+            self.launches += 1
+            return
         _lib.call("swmd_solve_f64_reset_done" if reset_done else "swmd_solve_f64",
                   dc.col_ptr.data_ptr(), dc.rows.data_ptr(),
                   dc.vals.data_ptr(), dc.n_cols, dc.order.data_ptr(), self.K.data_ptr(),

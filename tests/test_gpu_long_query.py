@@ -111,3 +111,55 @@ def test_column_blocks_are_bitwise_identical():
         got = np.concatenate([solver(sel, w, int(b[r]), int(b[r + 1]), cfg, None).wmd
                               for r in range(world)])
         assert np.array_equal(got, one), world
+
+
+def test_hot_row_entry_point_is_bitwise_the_plain_solve():
+    """swmd_solve_hot_f64 with the corpus's hot-row index (the K rows of the
+    most frequent vocabulary rows read from a shared-memory slab when
+    SWMD_CTA_HOT is set, else ignored) gives the bits of swmd_solve_f64."""
+    import torch
+
+    from paper_2107_06433_b200 import _lib
+    from paper_2107_06433_b200.device import DeviceCorpus, DeviceEmbeddings, device, stream_ptr
+    from paper_2107_06433_b200.solver import QueryPlan, SinkhornWorkspace
+
+    q, corpus, emb, _ = _case(99, 3000, 160, 5, 90, 200)
+    cfg = swmd.SolverConfig(lam=10.0, max_iter=15)
+    dev = device()
+    dc, de = DeviceCorpus.of(corpus, dev), DeviceEmbeddings.of(emb, dev)
+    sel, w = swmd.select_nonzero(q)
+    plan = QueryPlan(sel, w, dc, de, cfg, SinkhornWorkspace())
+    plan.enqueue_distances()
+    plan.enqueue_solve()
+    torch.cuda.synchronize()
+    want = plan.wmd.clone()
+    slot, ids = dc.hot_index()
+    assert ids is not None and int(slot[ids.long()].min()) == 0
+    counts = np.bincount(np.asarray(corpus.csc_index()[1]), minlength=3000)
+    assert counts[int(ids[0])] == counts.max()
+    plan.wmd.zero_()
+    _lib.call("swmd_err_reset", plan.err.data_ptr(), plan.stream)
+    _lib.call("swmd_solve_hot_f64", dc.col_ptr.data_ptr(), dc.rows.data_ptr(), dc.vals.data_ptr(),
+              dc.n_cols, dc.order.data_ptr(), plan.K.data_ptr(), plan.KM.data_ptr(),
+              plan.r_dev.data_ptr(), plan.v_r, plan.ldk, 0, cfg.max_iter, None, None,
+              plan.wmd.data_ptr(), dc.col_offset, dc.n_key, plan.group, dc.max_len,
+              plan.err.data_ptr(), plan.counter.data_ptr(), stream_ptr(dev), 0,
+              slot.data_ptr(), ids.data_ptr(), int(ids.numel()))
+    torch.cuda.synchronize()
+    assert torch.equal(plan.wmd, want)
+
+
+def test_suite_with_the_hot_row_slab_enabled():
+    """The slab variant is opt-in (SWMD_CTA_HOT=<rows>, read once per
+    process): rerun this file's solver cases in a child process with it on."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("SWMD_CTA_HOT_CHILD"):
+        pytest.skip("already the child run")
+    env = dict(os.environ, SWMD_CTA_HOT="48", SWMD_CTA_HOT_CHILD="1")
+    res = subprocess.run([sys.executable, "-m", "pytest", __file__, "-x", "-q", "-p", "no:cacheprovider",
+                          "-k", "row_width or staged_index or zero_denominator or tol_path or hot_row"],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
