@@ -163,3 +163,27 @@ def test_suite_with_the_hot_row_slab_enabled():
                           "-k", "row_width or staged_index or zero_denominator or tol_path or hot_row"],
                          env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+
+
+def test_empty_column_raises_the_reference_error(oracle_lib):
+    """A document with no words: x collapses to 0 after the first pass and the
+    reference's update_u check names the entry (solver.py:95-103)."""
+    rng = np.random.default_rng(5)
+    V, N, v_r = 600, 9, 70
+    emb = synth.normal_embeddings(rng, V, 16)
+    cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, 3, 30)
+    # drop every entry of column 4
+    keep = np.ones(rows.size, dtype=bool)
+    keep[cp[4]:cp[5]] = False
+    lens = np.diff(cp)
+    lens[4] = 0
+    cp2 = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    rows2, vals2 = rows[keep], vals[keep]
+    corpus = CsrMatrix.from_csc(V, N, cp2, rows2, vals2)
+    q = synth.zipf_query(rng, V, v_r)
+    cfg = swmd.SolverConfig(lam=2.0, max_iter=5)
+    with pytest.raises(swmd.DegeneracyError) as exc:
+        swmd.sinkhorn_wmd(q, corpus, emb, cfg)
+    with pytest.raises(oracle_lib.OracleDegeneracy) as want:
+        oracle_lib.solve(q, cp2, rows2, vals2, emb, lam=2.0, max_iter=5)
+    assert str(exc.value) == str(want.value)
