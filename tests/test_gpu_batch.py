@@ -85,3 +85,63 @@ def test_group_isolates_a_degenerate_query(oracle_lib):
     assert "zero denominator" in str(out[1])
     assert isinstance(out[0], swmd.SolverResult) and isinstance(out[2], swmd.SolverResult)
     assert np.array_equal(out[0].wmd, out[2].wmd)
+
+
+@pytest.mark.parametrize("V,dim,widths", [(300, 20, [5, 9]), (1000, 300, [64, 33, 8, 31]),
+                                          (129, 5, [3]), (2500, 17, [40] * 7), (257, 16, [12, 13])])
+def test_gram_kernels_agree(V, dim, widths):
+    """The tensor-core Gram (tcgen05 kind::tf32 with the 3xTF32 split, TMEM
+    accumulator) against the FFMA Gram on the same batch: K and K*M over
+    row / column / depth counts that are not multiples of the 128 x 128 x 16
+    tile, with and without a present-row list.  3xTF32 keeps fp32-level dot
+    products: |dK| <= 2e-5 K-scale (lam * dM), far inside the batch's 1e-4."""
+    import os
+
+    import torch
+
+    from paper_2107_06433_b200 import _lib
+    from paper_2107_06433_b200.device import device, stream_ptr
+
+    rng = np.random.default_rng(V + dim)
+    dev = device()
+    s = stream_ptr(dev)
+    emb = synth.normal_embeddings(rng, V, dim, np.float32)
+    ld = (dim + 3) // 4 * 4
+    E = torch.zeros((V, ld), dtype=torch.float32, device=dev)
+    E[:, :dim] = torch.from_numpy(emb).to(dev)
+    norms = torch.empty(V, dtype=torch.float32, device=dev)
+    _lib.call("swmd_row_norms_f32", E.data_ptr(), V, dim, ld, norms.data_ptr(), s)
+    words, col_word, off = [], [], 0
+    for w in widths:
+        sel = np.sort(rng.choice(V, size=w, replace=False))
+        blk = (w + 7) // 8 * 8
+        col_word += list(range(off, off + w)) + [-1] * (blk - w)
+        words += list(sel)
+        off += w
+    LD = len(col_word)
+    words_d = torch.tensor(words, dtype=torch.int64, device=dev)
+    col_d = torch.tensor(col_word, dtype=torch.int32, device=dev)
+    for present in (None, np.sort(rng.choice(V, size=max(1, (2 * V) // 3), replace=False))):
+        rl = torch.tensor(present, dtype=torch.int32, device=dev) if present is not None else None
+        outs = {}
+        for mode in ("ffma", "tc5"):
+            os.environ["SWMD_GRAM32"] = mode
+            K = torch.full((V, LD), -1.0, dtype=torch.float32, device=dev)
+            KM = torch.full((V, LD), -1.0, dtype=torch.float32, device=dev)
+            try:
+                _lib.call("swmd_cost_build_batch_f32", E.data_ptr(), V, dim, ld, words_d.data_ptr(),
+                          col_d.data_ptr(), LD, 10.0, norms.data_ptr(),
+                          rl.data_ptr() if rl is not None else None,
+                          int(rl.numel()) if rl is not None else 0, K.data_ptr(), KM.data_ptr(), s)
+                torch.cuda.synchronize()
+            finally:
+                os.environ.pop("SWMD_GRAM32", None)
+            outs[mode] = (K.cpu().numpy(), KM.cpu().numpy())
+        rows = np.arange(V) if present is None else present
+        for a, b in zip(outs["ffma"], outs["tc5"]):
+            assert np.array_equal(a == -1.0, b == -1.0)          # the same entries written
+            assert np.max(np.abs(a[rows] - b[rows])) <= 2e-5
+        # exact zeros: a word against itself, and padding columns
+        Kt = outs["tc5"][0]
+        pad = np.array(col_word) < 0
+        assert np.all(Kt[rows][:, pad] == 0.0)
