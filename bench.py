@@ -839,7 +839,9 @@ def run_batch_f32(args):
         "gpu_launches": int(batch_mod.last_launches * args.steps),
         "clocks": clock_info,
         "kernels": {"cost_build_ms": cost_ms, "solves_ms": solve_ms,
-                    "cost_build": "gram32_kernel (one launch for the batch)",
+                    "cost_build": "gram32_tc5_kernel: tcgen05.mma kind::tf32 x 3 (3xTF32), TMEM "
+                                  "accumulator, one launch for the batch (SWMD_GRAM32=ffma|mma: the "
+                                  "FFMA / mma.sync kernels)",
                     "solve": "reg_solve_mq<float>: one persistent launch per group of up to 4 "
                              "queries of one padded width, each claimed column solved for every "
                              "query of the group (CSC read once per group)",
