@@ -187,3 +187,40 @@ def test_empty_column_raises_the_reference_error(oracle_lib):
     with pytest.raises(oracle_lib.OracleDegeneracy) as want:
         oracle_lib.solve(q, cp2, rows2, vals2, emb, lam=2.0, max_iter=5)
     assert str(exc.value) == str(want.value)
+
+
+def test_randomised_long_queries_match_oracle(oracle_lib):
+    """Seeded sweep over what cta2_solve specialises on: v_r from 33 to 256
+    (1-4 chunks per lane, whole and clamped rows), column lengths from 1 to
+    ~600 (shorter than one CTA step, staged, past the staged arrays), lambda
+    from 0.5 to 30, 1 to 20 iterations; every case within 1e-9 of the oracle
+    with the same top-10, or the oracle's degeneracy message."""
+    from conftest import check_topk
+
+    rng = np.random.default_rng(20261021)
+    for case in range(24):
+        V = int(rng.integers(300, 3000))
+        N = int(rng.integers(1, 120))
+        dim = int(rng.choice([2, 8, 30, 64]))
+        kmin = int(rng.integers(1, 60))
+        kmax = min(V, kmin + int(rng.choice([0, 10, 90, 560])))
+        v_r = int(rng.integers(33, 257))
+        lam = float(rng.choice([0.5, 3.0, 10.0, 30.0]))
+        it = int(rng.integers(1, 21))
+        emb = synth.normal_embeddings(rng, V, dim)
+        cp, rows, vals = synth.zipf_corpus_csc(rng, V, N, kmin, kmax)
+        corpus = CsrMatrix.from_csc(V, N, cp, rows, vals)
+        q = synth.zipf_query(rng, V, min(v_r, V))
+        cfg = swmd.SolverConfig(lam=lam, max_iter=it)
+        try:
+            want = oracle_lib.solve(q, cp, rows, vals, emb, lam=lam, max_iter=it).wmd
+        except oracle_lib.OracleDegeneracy as exc:
+            with pytest.raises(swmd.DegeneracyError) as got_exc:
+                swmd.sinkhorn_wmd(q, corpus, emb, cfg)
+            assert str(got_exc.value) == str(exc), case
+            continue
+        got = swmd.sinkhorn_wmd(q, corpus, emb, cfg).wmd
+        assert max_rel_err(got, want) <= RTOL, (case, V, N, dim, kmin, kmax, v_r, lam, it)
+        k = min(10, N)
+        order = np.argsort(want, kind="stable")
+        check_topk(got, order[: k + 1], want[order[: k + 1]], k, ref_full=want)
