@@ -87,13 +87,16 @@ def test_group_isolates_a_degenerate_query(oracle_lib):
     assert np.array_equal(out[0].wmd, out[2].wmd)
 
 
-@pytest.mark.parametrize("V,dim,widths", [(300, 20, [5, 9]), (1000, 300, [64, 33, 8, 31]),
-                                          (129, 5, [3]), (2500, 17, [40] * 7), (257, 16, [12, 13])])
-def test_gram_kernels_agree(V, dim, widths):
+@pytest.mark.parametrize("V,dim,widths,trim", [(300, 20, [5, 9], 0), (1000, 300, [64, 33, 8, 31], 0),
+                                               (129, 5, [3], 0), (2500, 17, [40] * 7, 0),
+                                               (257, 16, [12, 13], 0), (400, 24, [9], 4),
+                                               (700, 40, [17, 20], 4)])
+def test_gram_kernels_agree(V, dim, widths, trim):
     """The tensor-core Gram (tcgen05 kind::tf32 with the 3xTF32 split, TMEM
     accumulator) against the FFMA Gram on the same batch: K and K*M over
-    row / column / depth counts that are not multiples of the 128 x 128 x 16
-    tile, with and without a present-row list.  3xTF32 keeps fp32-level dot
+    row / column / depth counts that are not multiples of the 128 x 256 x 16
+    tile (and row strides that rule out its 32-byte stores), with and without a
+    present-row list.  3xTF32 keeps fp32-level dot
     products: |dK| <= 2e-5 K-scale (lam * dM), far inside the batch's 1e-4."""
     import os
 
@@ -118,7 +121,11 @@ def test_gram_kernels_agree(V, dim, widths):
         col_word += list(range(off, off + w)) + [-1] * (blk - w)
         words += list(sel)
         off += w
+    if trim:                       # a row stride that is a multiple of 4 but not of 8
+        assert all(c < 0 for c in col_word[-trim:])
+        col_word = col_word[:-trim]
     LD = len(col_word)
+    assert LD % 4 == 0 and (trim == 0 or LD % 8 == 4)
     words_d = torch.tensor(words, dtype=torch.int64, device=dev)
     col_d = torch.tensor(col_word, dtype=torch.int32, device=dev)
     for present in (None, np.sort(rng.choice(V, size=max(1, (2 * V) // 3), replace=False))):
