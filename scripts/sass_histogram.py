@@ -12,7 +12,7 @@ import sys
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2107_06433_b200/libswmd.so"
 out = sys.argv[2] if len(sys.argv) > 2 else "profiles/r02_sass.json"
-WATCH = ["DMMA", "HMMA", "UTCMMA", "UTCHMMA", "UTMALDG", "UBLKCP", "SYNCS", "DFMA", "DADD", "DMUL",
+WATCH = ["DMMA", "HMMA", "UTCMMA", "UTCHMMA", "UTCBAR", "UTCATOMSWS", "LDTM", "UTMALDG", "UBLKCP", "SYNCS", "DFMA", "DADD", "DMUL",
          "FFMA", "MUFU", "SHFL", "LDS", "STS", "LDG", "STG", "LDGSTS", "ATOMG", "RED", "BAR",
          "UCGABAR", "MEMBAR", "BRA"]
 sass = subprocess.run(["cuobjdump", "-sass", lib], check=True, capture_output=True, text=True).stdout
@@ -36,6 +36,7 @@ for (name, cnt), dm in zip(kernels.items(), demangled):
     res[short] = {"instructions": total, **{k: cnt[k] for k in WATCH if cnt[k]}}
 keep = {k: v for k, v in res.items()
         if re.match(r"(void )?(cost_tmap_kernel|reg_solve<double, 20>|reg_solve<float|cta_solve<double, 8>|"
+                    r"cta2_solve<4|gram32_tc5_kernel|gram32_mma_kernel|reg_solve_mq<float, 48>|"
                     r"clu_solve<8>|gram32_kernel|unf_sddmm_kernel<20>|unf_spmm_kernel<20>|"
                     r"topk_kernel|csc_sort_kernel)", k.replace("void ", ""))}
 with open(out, "w") as f:
